@@ -1,0 +1,421 @@
+// gemm.cu -- persistent stream-K bf16 GEMM on 5th-gen tensor cores.
+//
+//   C[M,N] = A[M,K] . B[N,K]^T  (+bias) (relu) (+residual)
+//
+// A = activations (chunk tokens or decode rows), B = nn.Linear weights
+// [out, in]; both K-major, so every dense GEMM of the OPT/Llama layer is the
+// canonical "TN" UMMA problem.
+//
+// Structure (one CTA per SM, 192 threads):
+//   warp 0      TMA producer: A/B tiles -> 4..6-stage 128B-swizzled smem ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (128xBNx16)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused bias / ReLU /
+//               residual -> global; 2 TMEM accumulators so the epilogue of
+//               one tile overlaps the MMAs of the next
+//
+// Work split: the (tile, k-block) iteration space is divided evenly over the
+// persistent CTAs (stream-K).  A tile owned by one CTA is written directly;
+// a tile shared by several CTAs is reduced through an fp32 workspace with
+// float4 atomics, and the last contributor to arrive (per-tile counter)
+// applies the epilogue and re-zeroes the workspace.  Nobody ever waits on a
+// peer CTA, so the scheme is deadlock-free at any occupancy.  This fixes the
+// wave quantisation of M=512 chunk GEMMs (e.g. 80 tiles of 128x256 at
+// N=5120 on 148 SMs) and of skinny decode GEMMs alike.
+//
+// Tiles are numbered m-fastest so CTAs running concurrently share the same
+// weight panel: each weight byte is read from HBM once per GEMM and served
+// to the other m-tiles from L2.
+#include "tk_common.cuh"
+#include "tk_kernels.h"
+
+namespace tk {
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int BM = 128;
+  static constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+  static constexpr int THREADS = 192;
+};
+
+struct GemmArgs {
+  void* C;
+  const __nv_bfloat16* bias;
+  float* ws;
+  int* counters;
+  int M, N, K;
+  int epi;
+  int tiles_m, tiles_n, kbs;
+  long long total_iters;
+};
+
+__device__ __forceinline__ int owner_of(long long it, long long T, int G) {
+  // CTA c covers [floor(c*T/G), floor((c+1)*T/G))
+  return static_cast<int>(((it + 1) * G + T - 1) / T) - 1;
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_store(const GemmArgs& p, int row, int col0,
+                                               float (&v)[32]) {
+  if (row >= p.M) return;
+  if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_RELU || EPI == EPI_F32_BIAS_RESID) {
+    if (p.bias != nullptr) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        if (col0 + g * 8 < p.N) {
+          uint4 braw = __ldg(reinterpret_cast<const uint4*>(p.bias + col0 + g * 8));
+          const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&braw);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[g * 8 + j] += __bfloat162float(b[j]);
+        }
+      }
+    }
+  }
+  if constexpr (EPI == EPI_BF16_BIAS_RELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+  if constexpr (EPI == EPI_F32_BIAS_RESID || EPI == EPI_F32) {
+    float* out = reinterpret_cast<float*>(p.C) + static_cast<size_t>(row) * p.N + col0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      if (col0 + g * 4 < p.N) {
+        float4 o = make_float4(v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]);
+        if constexpr (EPI == EPI_F32_BIAS_RESID) {
+          float4 r = *reinterpret_cast<float4*>(out + g * 4);
+          o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+        }
+        *reinterpret_cast<float4*>(out + g * 4) = o;
+      }
+    }
+  } else {
+    __nv_bfloat16* out =
+        reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.N + col0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (col0 + g * 8 < p.N) {
+        uint4 o;
+        o.x = pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]);
+        o.y = pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]);
+        o.z = pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]);
+        o.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
+        *reinterpret_cast<uint4*>(out + g * 8) = o;
+      }
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
+    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                   const __grid_constant__ CUtensorMap tmap_b, const GemmArgs p) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + Cfg::STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const long long T = p.total_iters;
+  const int G = gridDim.x;
+  const long long it_begin = static_cast<long long>(blockIdx.x) * T / G;
+  const long long it_end = static_cast<long long>(blockIdx.x + 1) * T / G;
+  const int kbs = p.kbs;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      const uint64_t pol_a = l2_policy_evict_last();   // activations: reused by every n-tile
+      const uint64_t pol_b = l2_policy_evict_first();  // weights: streamed once per GEMM
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long i = it_begin; i < it_end;) {
+        const int tile = static_cast<int>(i / kbs);
+        const long long seg_end = min(it_end, static_cast<long long>(tile + 1) * kbs);
+        const int m_idx = tile % p.tiles_m;
+        const int n_idx = tile / p.tiles_m;
+        for (int kb = static_cast<int>(i - static_cast<long long>(tile) * kbs);
+             kb < static_cast<int>(seg_end - static_cast<long long>(tile) * kbs); ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sa + stage * Cfg::A_BYTES, &tmap_a, &full[stage], kb * Cfg::BK,
+                      m_idx * Cfg::BM, pol_a);
+          tma_load_2d(sb + stage * Cfg::B_BYTES, &tmap_b, &full[stage], kb * Cfg::BK,
+                      n_idx * BN, pol_b);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        i = seg_end;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(Cfg::BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (long long i = it_begin; i < it_end;) {
+        const int tile = static_cast<int>(i / kbs);
+        const long long seg_end = min(it_end, static_cast<long long>(tile + 1) * kbs);
+        const int nkb = static_cast<int>(seg_end - i);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int k = 0; k < nkb; ++k) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sa + stage * Cfg::A_BYTES);
+          const uint32_t b_addr = smem_u32(sb + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < Cfg::BK / 16; ++kk) {
+            umma_bf16(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                      idesc, (k > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        i = seg_end;
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_tile = static_cast<int>(quarter * 32 + lane);
+    const bool leader = (warp == 2 && lane == 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long i = it_begin; i < it_end;) {
+      const int tile = static_cast<int>(i / kbs);
+      const long long tile_first = static_cast<long long>(tile) * kbs;
+      const long long seg_end = min(it_end, tile_first + kbs);
+      const int m_idx = tile % p.tiles_m;
+      const int n_idx = tile / p.tiles_m;
+      const int row = m_idx * Cfg::BM + row_in_tile;
+      const int col_base = n_idx * BN;
+      const int contrib = owner_of(tile_first + kbs - 1, T, G) - owner_of(tile_first, T, G) + 1;
+
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((quarter * 32) << 16) + acc * BN;
+
+      if (contrib == 1) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, r);
+          tmem_wait_ld();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          epilogue_store<EPI>(p, row, col_base + c * 32, v);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else {
+        float* ws_row = p.ws + (static_cast<size_t>(tile) * Cfg::BM + row_in_tile) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            atomicAdd(reinterpret_cast<float4*>(ws_row + c * 32 + g * 4),
+                      make_float4(__uint_as_float(r[g * 4]), __uint_as_float(r[g * 4 + 1]),
+                                  __uint_as_float(r[g * 4 + 2]), __uint_as_float(r[g * 4 + 3])));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (leader) {
+          const int prev = atomicAdd(p.counters + tile, 1);
+          *last_flag = (prev == contrib - 1) ? 1 : 0;
+        }
+        named_bar_sync(1, 128);
+        if (*last_flag) {
+          __threadfence();
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            float v[32];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              float4 s = __ldcg(reinterpret_cast<const float4*>(ws_row + c * 32 + g * 4));
+              v[g * 4] = s.x; v[g * 4 + 1] = s.y; v[g * 4 + 2] = s.z; v[g * 4 + 3] = s.w;
+              __stcg(reinterpret_cast<float4*>(ws_row + c * 32 + g * 4),
+                     make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+            epilogue_store<EPI>(p, row, col_base + c * 32, v);
+          }
+          named_bar_sync(1, 128);
+          if (leader) atomicExch(p.counters + tile, 0);
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      i = seg_end;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+}
+
+// ------------------------------------------------------------------ host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// rows x cols bf16 row-major (cols = K contiguous), box = box_rows x 64, SW128.
+int make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                     uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  TK_CHECK(fn != nullptr, TK_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TK_CHECK(r == CUDA_SUCCESS, TK_ECUDA,
+           "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return TK_OK;
+}
+
+static int pick_bn(int N) { return N >= 1024 ? 256 : 128; }
+
+int64_t gemm_workspace_bytes(int M, int N, int K) {
+  const int bn = pick_bn(N);
+  const int64_t tiles = static_cast<int64_t>((M + 127) / 128) * ((N + bn - 1) / bn);
+  return tiles * 128 * bn * 4 + tiles * 4 + 256;
+}
+
+template <int BN, int EPI>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int grid,
+                       cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    TK_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<BN, EPI>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    configured = true;
+  }
+  gemm_tn_kernel<BN, EPI><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ta, tb, a);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+template <int BN>
+static int dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int grid,
+                        cudaStream_t s) {
+  switch (a.epi) {
+    case EPI_BF16: return launch_gemm<BN, EPI_BF16>(ta, tb, a, grid, s);
+    case EPI_BF16_BIAS: return launch_gemm<BN, EPI_BF16_BIAS>(ta, tb, a, grid, s);
+    case EPI_BF16_BIAS_RELU: return launch_gemm<BN, EPI_BF16_BIAS_RELU>(ta, tb, a, grid, s);
+    case EPI_F32_BIAS_RESID: return launch_gemm<BN, EPI_F32_BIAS_RESID>(ta, tb, a, grid, s);
+    case EPI_F32: return launch_gemm<BN, EPI_F32>(ta, tb, a, grid, s);
+  }
+  set_error("unknown gemm epilogue");
+  return TK_EINVAL;
+}
+
+int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, int N, int K,
+              int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas) {
+  TK_CHECK(M > 0 && N > 0 && K > 0, TK_EINVAL, "gemm: empty problem");
+  TK_CHECK(K % 64 == 0, TK_EINVAL, "gemm: K must be a multiple of 64");
+  TK_CHECK(N % 8 == 0, TK_EINVAL, "gemm: N must be a multiple of 8");
+  TK_CHECK(ws_bytes >= gemm_workspace_bytes(M, N, K), TK_EINVAL, "gemm: workspace too small");
+  const int bn = pick_bn(N);
+  CUtensorMap ta, tb;
+  int rc = make_tmap_kmajor(&ta, A, M, K, 128);
+  if (rc) return rc;
+  rc = make_tmap_kmajor(&tb, B, N, K, bn);
+  if (rc) return rc;
+  GemmArgs a;
+  a.C = C;
+  a.bias = static_cast<const __nv_bfloat16*>(bias);
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.epi = epi;
+  a.tiles_m = (M + 127) / 128;
+  a.tiles_n = (N + bn - 1) / bn;
+  a.kbs = K / 64;
+  const int64_t tiles = static_cast<int64_t>(a.tiles_m) * a.tiles_n;
+  a.total_iters = tiles * a.kbs;
+  a.ws = static_cast<float*>(workspace);
+  a.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(workspace) + tiles * 128 * bn * 4);
+  // Enough k-blocks per CTA to amortise the prologue; never more CTAs than SMs.
+  int grid = static_cast<int>(std::min<int64_t>(max_ctas > 0 ? max_ctas : kNumSMs,
+                                                std::max<int64_t>(1, a.total_iters / 4)));
+  if (tiles >= grid && tiles % grid == 0) grid = static_cast<int>(std::min<int64_t>(grid, tiles));
+  if (bn == 256) return dispatch_epi<256>(ta, tb, a, grid, stream);
+  return dispatch_epi<128>(ta, tb, a, grid, stream);
+}
+
+}  // namespace tk

@@ -1,0 +1,783 @@
+// kernels.cu -- the non-GEMM kernels of the chunked-prefill and decode paths.
+//
+//   embed_*            token (+ learned position, OPT offset 2) -> fp32 residual rows
+//   layernorm/rmsnorm  fp32 residual -> bf16 GEMM operand (one CTA per row)
+//   kv_write           fused QKV rows -> K/V into the request's pages (+RoPE for Llama)
+//   chunk_attention    K2: chunked-prefill attention, causal within each request slice
+//                      over the request's paged prefix; bf16 mma.sync tiles, online
+//                      softmax in fp32, cp.async double-buffered 64-token KV blocks
+//   decode_attention   K3: paged decode attention, split-KV over 256-token partitions,
+//                      128-bit coalesced page loads, warp-shuffle softmax, combine pass
+//   argmax             greedy token per row (first maximum, like torch.argmax)
+#include <cfloat>
+
+#include "tk_common.cuh"
+#include "tk_kernels.h"
+
+namespace tk {
+
+// ------------------------------------------------------------------ embeddings
+__global__ void embed_opt_kernel(const int32_t* __restrict__ ids, const TokenMeta* __restrict__ meta,
+                                 const __nv_bfloat16* __restrict__ tok,
+                                 const __nv_bfloat16* __restrict__ pos, float* __restrict__ out,
+                                 int hidden) {
+  const int t = blockIdx.x;
+  const int id = ids[t];
+  const int p = meta[t].pos + 2;  // OPTLearnedPositionalEmbedding offset
+  const __nv_bfloat16* te = tok + static_cast<size_t>(id) * hidden;
+  const __nv_bfloat16* pe = pos + static_cast<size_t>(p) * hidden;
+  float* o = out + static_cast<size_t>(t) * hidden;
+  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
+    uint4 a = *reinterpret_cast<const uint4*>(te + c);
+    uint4 b = *reinterpret_cast<const uint4*>(pe + c);
+    const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(&a);
+    const __nv_bfloat16* bv = reinterpret_cast<const __nv_bfloat16*>(&b);
+    float4 r0, r1;
+    r0.x = __bfloat162float(av[0]) + __bfloat162float(bv[0]);
+    r0.y = __bfloat162float(av[1]) + __bfloat162float(bv[1]);
+    r0.z = __bfloat162float(av[2]) + __bfloat162float(bv[2]);
+    r0.w = __bfloat162float(av[3]) + __bfloat162float(bv[3]);
+    r1.x = __bfloat162float(av[4]) + __bfloat162float(bv[4]);
+    r1.y = __bfloat162float(av[5]) + __bfloat162float(bv[5]);
+    r1.z = __bfloat162float(av[6]) + __bfloat162float(bv[6]);
+    r1.w = __bfloat162float(av[7]) + __bfloat162float(bv[7]);
+    *reinterpret_cast<float4*>(o + c) = r0;
+    *reinterpret_cast<float4*>(o + c + 4) = r1;
+  }
+}
+
+int launch_embed_opt(const int32_t* ids, const TokenMeta* meta, int n, const __nv_bfloat16* tok_emb,
+                     const __nv_bfloat16* pos_emb, float* resid, int hidden, cudaStream_t s) {
+  if (n == 0) return TK_OK;
+  embed_opt_kernel<<<n, 128, 0, s>>>(ids, meta, tok_emb, pos_emb, resid, hidden);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+__global__ void embed_plain_kernel(const int32_t* __restrict__ ids,
+                                   const __nv_bfloat16* __restrict__ tok, float* __restrict__ out,
+                                   int hidden) {
+  const int t = blockIdx.x;
+  const __nv_bfloat16* te = tok + static_cast<size_t>(ids[t]) * hidden;
+  float* o = out + static_cast<size_t>(t) * hidden;
+  for (int c = threadIdx.x; c < hidden; c += blockDim.x) o[c] = __bfloat162float(te[c]);
+}
+
+int launch_embed_llama(const int32_t* ids, int n, const __nv_bfloat16* tok_emb, float* resid,
+                       int hidden, cudaStream_t s) {
+  if (n == 0) return TK_OK;
+  embed_plain_kernel<<<n, 256, 0, s>>>(ids, tok_emb, resid, hidden);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+// ------------------------------------------------------------------ norms
+template <int kThreads>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float total = 0.f;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) total += red[i];
+  __syncthreads();
+  return total;
+}
+
+constexpr int kNormThreads = 256;
+constexpr int kNormMaxPer = 32;  // cols <= 8192
+
+template <bool kRms>
+__global__ void __launch_bounds__(kNormThreads)
+    norm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+                const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y, int cols,
+                float eps) {
+  __shared__ float red[kNormThreads / 32];
+  const float* xr = x + static_cast<size_t>(blockIdx.x) * cols;
+  __nv_bfloat16* yr = y + static_cast<size_t>(blockIdx.x) * cols;
+  float v[kNormMaxPer];
+  int n = 0;
+  float s = 0.f;
+  for (int c = threadIdx.x * 4; c < cols; c += kNormThreads * 4, n += 4) {
+    float4 q = *reinterpret_cast<const float4*>(xr + c);
+    v[n] = q.x; v[n + 1] = q.y; v[n + 2] = q.z; v[n + 3] = q.w;
+    s += q.x + q.y + q.z + q.w;
+  }
+  float mean = 0.f;
+  if (!kRms) mean = block_sum<kNormThreads>(s, red) / cols;
+  float ss = 0.f;
+  for (int i = 0; i < n; ++i) {
+    const float d = v[i] - mean;
+    ss += d * d;
+  }
+  const float rstd = rsqrtf(block_sum<kNormThreads>(ss, red) / cols + eps);
+  n = 0;
+  for (int c = threadIdx.x * 4; c < cols; c += kNormThreads * 4, n += 4) {
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float t = (v[n + j] - mean) * rstd * __bfloat162float(w[c + j]);
+      if (!kRms) t += __bfloat162float(b[c + j]);
+      o[j] = t;
+    }
+    uint2 pk;
+    pk.x = pack_bf16x2(o[0], o[1]);
+    pk.y = pack_bf16x2(o[2], o[3]);
+    *reinterpret_cast<uint2*>(yr + c) = pk;
+  }
+}
+
+int launch_layernorm(const float* x, const __nv_bfloat16* w, const __nv_bfloat16* b,
+                     __nv_bfloat16* y, int rows, int cols, float eps, cudaStream_t s) {
+  TK_CHECK(cols % 4 == 0 && cols <= kNormThreads * kNormMaxPer, TK_EINVAL,
+           "layernorm: cols must be a multiple of 4 and <= 8192");
+  if (rows == 0) return TK_OK;
+  norm_kernel<false><<<rows, kNormThreads, 0, s>>>(x, w, b, y, cols, eps);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+int launch_rmsnorm(const float* x, const __nv_bfloat16* w, __nv_bfloat16* y, int rows, int cols,
+                   float eps, cudaStream_t s) {
+  TK_CHECK(cols % 4 == 0 && cols <= kNormThreads * kNormMaxPer, TK_EINVAL,
+           "rmsnorm: cols must be a multiple of 4 and <= 8192");
+  if (rows == 0) return TK_OK;
+  norm_kernel<true><<<rows, kNormThreads, 0, s>>>(x, w, nullptr, y, cols, eps);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows,
+                                   int cols, float* __restrict__ out) {
+  const float* src = x + static_cast<size_t>(rows[blockIdx.x]) * cols;
+  float* dst = out + static_cast<size_t>(blockIdx.x) * cols;
+  for (int c = threadIdx.x * 4; c < cols; c += blockDim.x * 4)
+    *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
+}
+
+int launch_gather_rows_f32(const float* x, const int32_t* rows, int n, int cols, float* out,
+                           cudaStream_t s) {
+  if (n == 0) return TK_OK;
+  gather_rows_kernel<<<n, 256, 0, s>>>(x, rows, cols, out);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+// ------------------------------------------------------------------ KV page write
+// One CTA per token; threads move 16-byte chunks of K and V (and rotate Q/K
+// for Llama).  qkv row layout: [q(H*D) | k(H*D) | v(H*D)].
+__global__ void kv_write_kernel(__nv_bfloat16* __restrict__ qkv, const TokenMeta* __restrict__ meta,
+                                __nv_bfloat16* __restrict__ pool, KvGeom g, int layer,
+                                float q_scale, int rope, float rope_theta) {
+  const int t = blockIdx.x;
+  const TokenMeta m = meta[t];
+  const int HD = g.n_heads * g.head_dim;
+  __nv_bfloat16* row = qkv + static_cast<size_t>(t) * 3 * HD;
+  if (rope) {
+    // rotate_half convention: pairs (d, d + D/2) within each head.
+    const int half = g.head_dim / 2;
+    for (int i = threadIdx.x; i < g.n_heads * half; i += blockDim.x) {
+      const int h = i / half, d = i % half;
+      const float inv = powf(rope_theta, -2.f * d / g.head_dim);
+      float sn, cs;
+      sincosf(m.pos * inv, &sn, &cs);
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        __nv_bfloat16* base = row + part * HD + h * g.head_dim;
+        const float x0 = __bfloat162float(base[d]);
+        const float x1 = __bfloat162float(base[d + half]);
+        base[d] = __float2bfloat16(x0 * cs - x1 * sn);
+        base[d + half] = __float2bfloat16(x1 * cs + x0 * sn);
+      }
+    }
+    __syncthreads();
+  }
+  if (q_scale != 1.f) {
+    for (int i = threadIdx.x; i < HD; i += blockDim.x)
+      row[i] = __float2bfloat16(__bfloat162float(row[i]) * q_scale);
+  }
+  const int chunks = HD / 8;
+  for (int i = threadIdx.x; i < 2 * chunks; i += blockDim.x) {
+    const int kv = i / chunks;
+    const int c = i % chunks;
+    const int h = (c * 8) / g.head_dim;
+    const int d = (c * 8) % g.head_dim;
+    const uint4 val = *reinterpret_cast<const uint4*>(row + (1 + kv) * HD + c * 8);
+    *reinterpret_cast<uint4*>(pool + g.offset(m.page, layer, kv, h, m.slot) + d) = val;
+  }
+}
+
+int launch_kv_write(__nv_bfloat16* qkv, const TokenMeta* meta, int n, __nv_bfloat16* pool,
+                    KvGeom g, int layer, float q_scale, int rope, float rope_theta,
+                    cudaStream_t s) {
+  if (n == 0) return TK_OK;
+  kv_write_kernel<<<n, 256, 0, s>>>(qkv, meta, pool, g, layer, q_scale, rope, rope_theta);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+// ------------------------------------------------------------------ chunk attention (K2)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t sz = valid ? 16u : 0u;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(sz)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int D>
+__global__ void __launch_bounds__(128)
+    chunk_attn_kernel(const __nv_bfloat16* __restrict__ q, int q_stride,
+                      __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ pool,
+                      KvGeom g, int layer, const AttnWork* __restrict__ work,
+                      const tk_slice* __restrict__ slices, const int32_t* __restrict__ bt,
+                      float scale_log2) {
+  constexpr int BKV = 64;
+  constexpr int CH = D / 8;  // 16-byte chunks per row
+  constexpr int TILE = BKV * D;
+  extern __shared__ __align__(128) uint8_t sm[];
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(sm);  // [2][64][D]
+  __nv_bfloat16* sV = sK + 2 * TILE;                           // [2][64][D]
+
+  const AttnWork w = work[blockIdx.x];
+  const int head = blockIdx.y;
+  const tk_slice sl = slices[w.slice];
+  const int32_t* pages = bt + sl.bt_offset;
+  const int kv_end = w.pos0 + w.nrows;  // keys [0, kv_end) may be needed
+  const int n_blocks = (kv_end + BKV - 1) / BKV;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int pt = g.page_tokens;
+
+  auto load_block = [&](int j, int buf) {
+    __nv_bfloat16* dk = sK + buf * TILE;
+    __nv_bfloat16* dv = sV + buf * TILE;
+    for (int i = tid; i < BKV * CH; i += 128) {
+      const int r = i / CH, c = i % CH;
+      const int p = j * BKV + r;
+      const bool valid = p < kv_end;
+      const int page = valid ? pages[p / pt] : 0;
+      const size_t off = valid ? g.offset(page, layer, 0, head, p % pt) : 0;
+      const int sw = r * D + ((c ^ (r & 7)) * 8);
+      cp_async16(dk + sw, pool + off + c * 8, valid);
+      const size_t offv = valid ? g.offset(page, layer, 1, head, p % pt) : 0;
+      cp_async16(dv + sw, pool + offv + c * 8, valid);
+    }
+  };
+
+  load_block(0, 0);
+  cp_async_commit();
+
+  // Q fragments (16 rows per warp) straight from global.
+  uint32_t qa[D / 16][4];
+  const int r_lo = warp * 16 + gq, r_hi = r_lo + 8;
+  {
+    const __nv_bfloat16* q_lo = q + static_cast<size_t>(w.row0 + r_lo) * q_stride + head * D;
+    const __nv_bfloat16* q_hi = q + static_cast<size_t>(w.row0 + r_hi) * q_stride + head * D;
+    const bool v_lo = r_lo < w.nrows, v_hi = r_hi < w.nrows;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+      const int c = ks * 16 + tq * 2;
+      qa[ks][0] = v_lo ? *reinterpret_cast<const uint32_t*>(q_lo + c) : 0u;
+      qa[ks][1] = v_hi ? *reinterpret_cast<const uint32_t*>(q_hi + c) : 0u;
+      qa[ks][2] = v_lo ? *reinterpret_cast<const uint32_t*>(q_lo + c + 8) : 0u;
+      qa[ks][3] = v_hi ? *reinterpret_cast<const uint32_t*>(q_hi + c + 8) : 0u;
+    }
+  }
+  const int qp_lo = w.pos0 + r_lo, qp_hi = w.pos0 + r_hi;
+
+  float acc[D / 8][4];
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+
+  for (int j = 0; j < n_blocks; ++j) {
+    const int buf = j & 1;
+    if (j + 1 < n_blocks) load_block(j + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+
+    const uint32_t kbase = smem_u32(sK + buf * TILE);
+    const uint32_t vbase = smem_u32(sV + buf * TILE);
+    // S = Q K^T : 16 x 64 per warp
+    float s[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+#pragma unroll
+      for (int nt = 0; nt < 8; nt += 2) {
+        // matrices: (nt, chunk 2ks), (nt, 2ks+1), (nt+1, 2ks), (nt+1, 2ks+1)
+        const int mi = lane >> 3;
+        const int row = (nt + (mi >> 1)) * 8 + (lane & 7);
+        const int chunk = ks * 2 + (mi & 1);
+        const uint32_t addr = kbase + (row * D + ((chunk ^ (row & 7)) * 8)) * 2;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(addr, b0, b1, b2, b3);
+        mma_bf16_16816(s[nt], qa[ks], b0, b1);
+        mma_bf16_16816(s[nt + 1], qa[ks], b2, b3);
+      }
+    }
+    // causal mask (also hides keys beyond kv_end, which are zero-filled)
+    const int kp0 = j * BKV;
+    if (kp0 + BKV - 1 > w.pos0 + warp * 16) {
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const int kp = kp0 + nt * 8 + tq * 2;
+        if (kp > qp_lo) s[nt][0] = -INFINITY;
+        if (kp + 1 > qp_lo) s[nt][1] = -INFINITY;
+        if (kp > qp_hi) s[nt][2] = -INFINITY;
+        if (kp + 1 > qp_hi) s[nt][3] = -INFINITY;
+      }
+    }
+    // online softmax (rows lo / hi; reduce across the 4 lanes of a quad)
+    float mx_lo = m_lo, mx_hi = m_hi;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      mx_lo = fmaxf(mx_lo, fmaxf(s[nt][0], s[nt][1]) * scale_log2);
+      mx_hi = fmaxf(mx_hi, fmaxf(s[nt][2], s[nt][3]) * scale_log2);
+    }
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+    const float base_lo = (mx_lo == -INFINITY) ? 0.f : mx_lo;
+    const float base_hi = (mx_hi == -INFINITY) ? 0.f : mx_hi;
+    const float corr_lo = exp2f(m_lo - base_lo);
+    const float corr_hi = exp2f(m_hi - base_hi);
+    m_lo = mx_lo;
+    m_hi = mx_hi;
+    float sum_lo = 0.f, sum_hi = 0.f;
+    uint32_t pa[4][4];  // P as A fragments, 4 k-steps of 16 keys
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = exp2f(s[nt][0] * scale_log2 - base_lo);
+      const float p1 = exp2f(s[nt][1] * scale_log2 - base_lo);
+      const float p2 = exp2f(s[nt][2] * scale_log2 - base_hi);
+      const float p3 = exp2f(s[nt][3] * scale_log2 - base_hi);
+      sum_lo += p0 + p1;
+      sum_hi += p2 + p3;
+      const int ks = nt >> 1;
+      if ((nt & 1) == 0) {
+        pa[ks][0] = pack_bf16x2(p0, p1);
+        pa[ks][1] = pack_bf16x2(p2, p3);
+      } else {
+        pa[ks][2] = pack_bf16x2(p0, p1);
+        pa[ks][3] = pack_bf16x2(p2, p3);
+      }
+    }
+    l_lo = l_lo * corr_lo + sum_lo;
+    l_hi = l_hi * corr_hi + sum_hi;
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      acc[i][0] *= corr_lo;
+      acc[i][1] *= corr_lo;
+      acc[i][2] *= corr_hi;
+      acc[i][3] *= corr_hi;
+    }
+    // O += P V
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+      for (int nt = 0; nt < D / 8; nt += 2) {
+        // matrices: (keys 16ks+0..7, dchunk nt), (16ks+8.., nt), (16ks.., nt+1), (16ks+8.., nt+1)
+        const int mi = lane >> 3;
+        const int row = ks * 16 + (mi & 1) * 8 + (lane & 7);
+        const int chunk = nt + (mi >> 1);
+        const uint32_t addr = vbase + (row * D + ((chunk ^ (row & 7)) * 8)) * 2;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(addr, b0, b1, b2, b3);
+        mma_bf16_16816(acc[nt], pa[ks], b0, b1);
+        mma_bf16_16816(acc[nt + 1], pa[ks], b2, b3);
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  // finalize: quad-reduce row sums, normalise, store bf16
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
+  l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
+  l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
+  const float inv_lo = l_lo > 0.f ? 1.f / l_lo : 0.f;
+  const float inv_hi = l_hi > 0.f ? 1.f / l_hi : 0.f;
+  const int HD = g.n_heads * D;
+  if (r_lo < w.nrows) {
+    __nv_bfloat16* out = o + static_cast<size_t>(w.row0 + r_lo) * HD + head * D;
+#pragma unroll
+    for (int nt = 0; nt < D / 8; ++nt)
+      *reinterpret_cast<uint32_t*>(out + nt * 8 + tq * 2) =
+          pack_bf16x2(acc[nt][0] * inv_lo, acc[nt][1] * inv_lo);
+  }
+  if (r_hi < w.nrows) {
+    __nv_bfloat16* out = o + static_cast<size_t>(w.row0 + r_hi) * HD + head * D;
+#pragma unroll
+    for (int nt = 0; nt < D / 8; ++nt)
+      *reinterpret_cast<uint32_t*>(out + nt * 8 + tq * 2) =
+          pack_bf16x2(acc[nt][2] * inv_hi, acc[nt][3] * inv_hi);
+  }
+}
+
+int build_attn_work(const tk_slice* slices, int n_slices, AttnWork* out, int cap) {
+  int n = 0, row = 0;
+  for (int i = 0; i < n_slices; ++i) {
+    for (int r = 0; r < slices[i].len; r += 64) {
+      if (n >= cap) return -1;
+      out[n].slice = i;
+      out[n].row0 = row + r;
+      out[n].nrows = min(64, slices[i].len - r);
+      out[n].pos0 = slices[i].start + r;
+      ++n;
+    }
+    row += slices[i].len;
+  }
+  return n;
+}
+
+int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloat16* o,
+                                const __nv_bfloat16* pool, KvGeom g, int layer,
+                                const AttnWork* work, int n_work, const tk_slice* slices_dev,
+                                const int32_t* bt_dev, float scale, cudaStream_t s) {
+  TK_CHECK(g.head_dim == 128 || g.head_dim == 64, TK_EUNSUPPORTED,
+           "chunk attention: head_dim must be 64 or 128");
+  TK_CHECK(64 % g.page_tokens == 0 || g.page_tokens % 64 == 0, TK_EINVAL,
+           "chunk attention: page_tokens must divide 64 or be a multiple of it");
+  if (n_work == 0) return TK_OK;
+  const float scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(n_work, g.n_heads);
+  if (g.head_dim == 128) {
+    const int smem = 4 * 64 * 128 * 2;
+    static bool cfg = false;
+    if (!cfg) {
+      TK_CUDA(cudaFuncSetAttribute(chunk_attn_kernel<128>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cfg = true;
+    }
+    chunk_attn_kernel<128><<<grid, 128, smem, s>>>(q, q_stride, o, pool, g, layer, work, slices_dev,
+                                                   bt_dev, scale_log2);
+  } else {
+    const int smem = 4 * 64 * 64 * 2;
+    chunk_attn_kernel<64><<<grid, 128, smem, s>>>(q, q_stride, o, pool, g, layer, work, slices_dev,
+                                                  bt_dev, scale_log2);
+  }
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+// ------------------------------------------------------------------ paged decode attention (K3)
+constexpr int kDecSplitTokens = 256;
+
+// grid (splits, heads, batch), 128 threads; each warp walks pages of the split.
+// Lane l owns dims [(l%16)*8, +8) of token parity l/16 inside each 16-token load
+// group; partial (m, l, acc) of the 4 warps are merged in smem.
+template <int D>
+__global__ void __launch_bounds__(128)
+    decode_attn_kernel(const __nv_bfloat16* __restrict__ q, int q_stride,
+                       __nv_bfloat16* __restrict__ o,
+                       const __nv_bfloat16* __restrict__ pool, KvGeom g, int layer,
+                       const int32_t* __restrict__ bt, int bt_stride,
+                       const int32_t* __restrict__ ctx_lens, float scale_log2,
+                       float* __restrict__ ws, int max_splits) {
+  static_assert(D == 128, "decode attention: head_dim 128");
+  const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+  const int ctx = ctx_lens[b];
+  const int n_splits = (ctx + kDecSplitTokens - 1) / kDecSplitTokens;
+  if (split >= n_splits) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, dl = (lane & 15) * 8;
+  const int pt = g.page_tokens;  // 16
+  const int t0 = split * kDecSplitTokens;
+  const int t1 = min(ctx, t0 + kDecSplitTokens);
+
+  float qv[8];
+  {
+    const uint4 raw = *reinterpret_cast<const uint4*>(
+        q + static_cast<size_t>(b) * q_stride + head * D + dl);
+    const __nv_bfloat16* qb = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qv[i] = __bfloat162float(qb[i]) * scale_log2;
+  }
+  float m = -INFINITY, l = 0.f, acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+
+  const int32_t* pages = bt + static_cast<size_t>(b) * bt_stride;
+  for (int base = t0 + warp * pt; base < t1; base += 4 * pt) {
+    const int page = pages[base / pt];
+    const __nv_bfloat16* kp = pool + g.offset(page, layer, 0, head, 0);
+    const __nv_bfloat16* vp = pool + g.offset(page, layer, 1, head, 0);
+    uint4 kr[8], vr[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int tok = 2 * i + half;
+      kr[i] = __ldg(reinterpret_cast<const uint4*>(kp + tok * D + dl));
+      vr[i] = __ldg(reinterpret_cast<const uint4*>(vp + tok * D + dl));
+    }
+    float sc[8];
+    float pmax = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(&kr[i]);
+      float d = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) d += qv[e] * __bfloat162float(kb[e]);
+      d += __shfl_xor_sync(0xffffffffu, d, 8);
+      d += __shfl_xor_sync(0xffffffffu, d, 4);
+      d += __shfl_xor_sync(0xffffffffu, d, 2);
+      d += __shfl_xor_sync(0xffffffffu, d, 1);
+      const int tok = base + 2 * i + half;
+      sc[i] = tok < t1 ? d : -INFINITY;
+      pmax = fmaxf(pmax, sc[i]);
+    }
+    pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 16));
+    const float mn = fmaxf(m, pmax);
+    const float corr = exp2f(m - mn);
+    l *= corr;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= corr;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      // slots past the context may hold stale bytes (even NaN patterns): skip them
+      if (base + 2 * i + half < t1) {
+        const float p = exp2f(sc[i] - mn);
+        l += p;
+        const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&vr[i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += p * __bfloat162float(vb[e]);
+      }
+    }
+    m = mn;
+  }
+  // merge the two token-parity halves of the warp (same m)
+  l += __shfl_xor_sync(0xffffffffu, l, 16);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+
+  // merge 4 warps
+  __shared__ float s_m[4], s_l[4];
+  __shared__ float s_acc[4][D];
+  if (lane == 0) {
+    s_m[warp] = m;
+    s_l[warp] = l;
+  }
+  if (half == 0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s_acc[warp][dl + e] = acc[e];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float M = fmaxf(fmaxf(s_m[0], s_m[1]), fmaxf(s_m[2], s_m[3]));
+    float L = 0.f;
+    float w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      w[i] = (s_m[i] == -INFINITY) ? 0.f : exp2f(s_m[i] - M);
+      L += s_l[i] * w[i];
+    }
+    for (int d = lane; d < D; d += 32) {
+      const float a = s_acc[0][d] * w[0] + s_acc[1][d] * w[1] + s_acc[2][d] * w[2] +
+                      s_acc[3][d] * w[3];
+      if (n_splits == 1) {
+        o[(static_cast<size_t>(b) * g.n_heads + head) * D + d] = __float2bfloat16(a / L);
+      } else {
+        float* part = ws + ((static_cast<size_t>(b) * g.n_heads + head) * max_splits + split) * (D + 2);
+        part[d] = a;
+        if (d == 0) {
+          part[D] = M;
+          part[D + 1] = L;
+        }
+      }
+    }
+  }
+}
+
+template <int D>
+__global__ void decode_combine_kernel(__nv_bfloat16* __restrict__ o, int n_heads,
+                                      const int32_t* __restrict__ ctx_lens,
+                                      const float* __restrict__ ws, int max_splits) {
+  const int head = blockIdx.x, b = blockIdx.y;
+  const int n_splits = (ctx_lens[b] + kDecSplitTokens - 1) / kDecSplitTokens;
+  if (n_splits <= 1) return;
+  const float* parts = ws + (static_cast<size_t>(b) * n_heads + head) * max_splits * (D + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < n_splits; ++s) M = fmaxf(M, parts[s * (D + 2) + D]);
+  float L = 0.f;
+  for (int s = 0; s < n_splits; ++s)
+    L += parts[s * (D + 2) + D + 1] * exp2f(parts[s * (D + 2) + D] - M);
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float a = 0.f;
+    for (int s = 0; s < n_splits; ++s) a += parts[s * (D + 2) + d] * exp2f(parts[s * (D + 2) + D] - M);
+    o[(static_cast<size_t>(b) * n_heads + head) * D + d] = __float2bfloat16(a / L);
+  }
+}
+
+int64_t decode_attention_workspace_bytes(int batch, int n_heads, int head_dim, int max_ctx) {
+  const int splits = (max_ctx + kDecSplitTokens - 1) / kDecSplitTokens;
+  return static_cast<int64_t>(batch) * n_heads * splits * (head_dim + 2) * 4;
+}
+
+int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16* o,
+                            const __nv_bfloat16* pool,
+                            KvGeom g, int layer, const int32_t* block_tables, int bt_stride,
+                            const int32_t* ctx_lens, int batch, int max_ctx, float scale,
+                            void* workspace, int64_t ws_bytes, cudaStream_t s) {
+  TK_CHECK(g.head_dim == 128, TK_EUNSUPPORTED, "decode attention: head_dim must be 128");
+  TK_CHECK(g.page_tokens == 16, TK_EUNSUPPORTED, "decode attention: page_tokens must be 16");
+  TK_CHECK(ws_bytes >= decode_attention_workspace_bytes(batch, g.n_heads, g.head_dim, max_ctx),
+           TK_EINVAL, "decode attention: workspace too small");
+  if (batch == 0 || max_ctx == 0) return TK_OK;
+  const int splits = (max_ctx + kDecSplitTokens - 1) / kDecSplitTokens;
+  const float scale_log2 = scale * 1.4426950408889634f;
+  decode_attn_kernel<128><<<dim3(splits, g.n_heads, batch), 128, 0, s>>>(
+      q, q_stride, o, pool, g, layer, block_tables, bt_stride, ctx_lens, scale_log2,
+      static_cast<float*>(workspace), splits);
+  TK_CUDA(cudaGetLastError());
+  if (splits > 1) {
+    decode_combine_kernel<128><<<dim3(g.n_heads, batch), 128, 0, s>>>(
+        o, g.n_heads, ctx_lens, static_cast<const float*>(workspace), splits);
+    TK_CUDA(cudaGetLastError());
+  }
+  return TK_OK;
+}
+
+// ------------------------------------------------------------------ argmax
+__global__ void argmax_kernel(const float* __restrict__ x, int cols, int stride,
+                              int32_t* __restrict__ out) {
+  const float* row = x + static_cast<size_t>(blockIdx.x) * stride;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float v = row[c];
+    if (v > best || (v == best && c < idx)) {
+      best = v;
+      idx = c;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
+    if (ob > best || (ob == best && oi < idx)) {
+      best = ob;
+      idx = oi;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sb[w] = best;
+    si[w] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) {
+      if (sb[i] > best || (sb[i] == best && si[i] < idx)) {
+        best = sb[i];
+        idx = si[i];
+      }
+    }
+    out[blockIdx.x] = idx;
+  }
+}
+
+int launch_argmax_strided(const float* logits, int rows, int cols, int stride, int32_t* out,
+                          cudaStream_t s) {
+  if (rows == 0) return TK_OK;
+  argmax_kernel<<<rows, 1024, 0, s>>>(logits, cols, stride, out);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+// ------------------------------------------------------------------ init / elementwise
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void init_normal_kernel(__nv_bfloat16* w, int64_t n, uint64_t seed, float std) {
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 2; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x * 2) {
+    const uint64_t r = splitmix64(seed ^ (static_cast<uint64_t>(i) * 0xD1B54A32D192ED03ull));
+    const float u1 = (static_cast<float>(r >> 40) + 1.f) * (1.f / 16777216.f);
+    const float u2 = static_cast<float>((r >> 16) & 0xFFFFFF) * (1.f / 16777216.f);
+    const float rad = sqrtf(-2.f * logf(u1)) * std;
+    float sn, cs;
+    sincospif(2.f * u2, &sn, &cs);
+    w[i] = __float2bfloat16(rad * cs);
+    if (i + 1 < n) w[i + 1] = __float2bfloat16(rad * sn);
+  }
+}
+
+int launch_init_normal(__nv_bfloat16* w, int64_t n, uint64_t seed, float std, cudaStream_t s) {
+  if (n == 0) return TK_OK;
+  init_normal_kernel<<<kNumSMs * 8, 256, 0, s>>>(w, n, seed, std);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+__global__ void fill_kernel(__nv_bfloat16* w, int64_t n, float v) {
+  const __nv_bfloat16 b = __float2bfloat16(v);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    w[i] = b;
+}
+
+int launch_fill(__nv_bfloat16* w, int64_t n, float value, cudaStream_t s) {
+  if (n == 0) return TK_OK;
+  fill_kernel<<<kNumSMs * 4, 256, 0, s>>>(w, n, value);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+__global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out,
+                              int ffn) {
+  const int t = blockIdx.x;
+  const __nv_bfloat16* row = gu + static_cast<size_t>(t) * 2 * ffn;
+  for (int c = threadIdx.x; c < ffn; c += blockDim.x) {
+    const float gt = __bfloat162float(row[c]);
+    const float up = __bfloat162float(row[ffn + c]);
+    out[static_cast<size_t>(t) * ffn + c] = __float2bfloat16(gt / (1.f + __expf(-gt)) * up);
+  }
+}
+
+int launch_swiglu(const __nv_bfloat16* gate_up, __nv_bfloat16* out, int n, int ffn,
+                  cudaStream_t s) {
+  if (n == 0) return TK_OK;
+  swiglu_kernel<<<n, 256, 0, s>>>(gate_up, out, ffn);
+  TK_CUDA(cudaGetLastError());
+  return TK_OK;
+}
+
+}  // namespace tk

@@ -1,0 +1,87 @@
+// tk_kernels.h -- internal launchers shared by the runtime (runtime.cu) and
+// the raw C-ABI entry points.  All take device pointers and a stream.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tetri.h"
+
+namespace tk {
+
+enum Epi : int {
+  EPI_BF16 = 0,            // C bf16 = acc
+  EPI_BF16_BIAS = 1,       // C bf16 = acc + bias
+  EPI_BF16_BIAS_RELU = 2,  // C bf16 = relu(acc + bias)
+  EPI_F32_BIAS_RESID = 3,  // C fp32 += acc + bias (residual stream, in place)
+  EPI_F32 = 4,             // C fp32 = acc (logits)
+};
+
+int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, int N, int K,
+              int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas = 0);
+int64_t gemm_workspace_bytes(int M, int N, int K);
+
+// Page-major KV pool geometry: [page][layer][2][heads][page_tokens][head_dim] bf16.
+struct KvGeom {
+  int n_layers, n_heads, head_dim, page_tokens;
+  __host__ __device__ size_t page_elems() const {
+    return static_cast<size_t>(n_layers) * 2 * n_heads * page_tokens * head_dim;
+  }
+  // element offset of (page, layer, kv, head, slot, 0)
+  __host__ __device__ size_t offset(int page, int layer, int kv, int head, int slot) const {
+    return (((static_cast<size_t>(page) * n_layers + layer) * 2 + kv) * n_heads + head) *
+               static_cast<size_t>(page_tokens) * head_dim +
+           static_cast<size_t>(slot) * head_dim;
+  }
+};
+
+// Per-token row metadata of a chunk, built on the host from tk_slice[]:
+// position in its request, and the page / slot its K/V goes to.
+struct TokenMeta {
+  int32_t pos;
+  int32_t page;
+  int32_t slot;
+  int32_t slice;
+};
+
+int launch_embed_opt(const int32_t* ids, const TokenMeta* meta, int n, const __nv_bfloat16* tok_emb,
+                     const __nv_bfloat16* pos_emb, float* resid, int hidden, cudaStream_t s);
+int launch_embed_llama(const int32_t* ids, int n, const __nv_bfloat16* tok_emb, float* resid,
+                       int hidden, cudaStream_t s);
+int launch_layernorm(const float* x, const __nv_bfloat16* w, const __nv_bfloat16* b,
+                     __nv_bfloat16* y, int rows, int cols, float eps, cudaStream_t s);
+int launch_rmsnorm(const float* x, const __nv_bfloat16* w, __nv_bfloat16* y, int rows, int cols,
+                   float eps, cudaStream_t s);
+int launch_gather_rows_f32(const float* x, const int32_t* rows, int n, int cols, float* out,
+                           cudaStream_t s);
+// qkv [n, 3*H*D] bf16 (q scaled in place by q_scale) -> K,V into pages.
+int launch_kv_write(__nv_bfloat16* qkv, const TokenMeta* meta, int n, __nv_bfloat16* pool,
+                    KvGeom g, int layer, float q_scale, int rope, float rope_theta,
+                    cudaStream_t s);
+struct AttnWork {
+  int32_t slice;
+  int32_t row0;   // chunk row of the first query of this 64-row block
+  int32_t nrows;  // <= 64
+  int32_t pos0;   // position of that query in its request
+};
+// Host: split each slice into <=64-row query blocks; returns count or -1.
+int build_attn_work(const tk_slice* slices, int n_slices, AttnWork* out, int cap);
+int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloat16* o,
+                                const __nv_bfloat16* pool, KvGeom g, int layer,
+                                const AttnWork* work, int n_work, const tk_slice* slices_dev,
+                                const int32_t* bt_dev, float scale, cudaStream_t s);
+int64_t decode_attention_workspace_bytes(int batch, int n_heads, int head_dim, int max_ctx);
+int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16* o,
+                            const __nv_bfloat16* pool,
+                            KvGeom g, int layer, const int32_t* block_tables, int bt_stride,
+                            const int32_t* ctx_lens, int batch, int max_ctx, float scale,
+                            void* workspace, int64_t ws_bytes, cudaStream_t s);
+int launch_argmax_strided(const float* logits, int rows, int cols, int stride, int32_t* out,
+                          cudaStream_t s);
+int launch_init_normal(__nv_bfloat16* w, int64_t n, uint64_t seed, float std, cudaStream_t s);
+int launch_fill(__nv_bfloat16* w, int64_t n, float value, cudaStream_t s);
+int launch_swiglu(const __nv_bfloat16* gate_up, __nv_bfloat16* out, int n, int ffn,
+                  cudaStream_t s);
+
+}  // namespace tk

@@ -1,0 +1,160 @@
+"""Kernel-level parity on the B200: each sm_100a kernel against a plain torch
+fp32 reference of the same op (the floating-point tier of the oracle).
+
+Tolerances are bf16 ones: outputs are rounded to bf16 (8 bits of mantissa,
+relative step 2^-8 = 0.0039), accumulations are fp32.
+"""
+
+import pytest
+import torch
+
+from paper_2401_11181_b200 import native
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    native.load()
+
+
+def _rel_err(x, ref):
+    return ((x.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-6)).item()
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (128, 256, 64),      # one tile, one k-block
+    (512, 5120, 5120),   # OPT-13B O-proj at ChunkSize 512
+    (512, 15360, 5120),  # fused QKV
+    (300, 1024, 768),    # ragged M (TMA zero-fill, masked rows)
+    (7, 50272, 256),     # LM-head-like: N not a multiple of the tile
+    (33, 3072, 768),     # decode-sized M, BN=256, stream-K split
+    (64, 768, 3072),     # BN=128 path
+    (512, 48, 768),      # classifier head (N=48)
+])
+def test_gemm_matches_fp32(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    ref = a.float() @ b.float().t()
+    out = native.gemm(a, b, epilogue=native.EPI_F32)
+    torch.cuda.synchronize()
+    assert _rel_err(out, ref) < 2e-3
+    bias = (torch.randn(N, device="cuda", generator=g)).bfloat16()
+    out2 = native.gemm(a, b, bias=bias, epilogue=native.EPI_BF16_BIAS_RELU)
+    ref2 = torch.relu(ref + bias.float())
+    assert _rel_err(out2, ref2) < 1e-2
+
+
+def test_gemm_residual_epilogue_and_workspace_reuse():
+    M, N, K = 512, 5120, 20480  # FC2 shape; several CTAs share each tile
+    g = torch.Generator(device="cuda").manual_seed(1)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.02).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    resid = torch.randn(M, N, device="cuda", generator=g)
+    ws = None
+    for _ in range(3):  # the stream-K workspace must come back zeroed each time
+        out = resid.clone()
+        import ctypes
+        nbytes = ctypes.c_int64()
+        native.check(native.load().tk_gemm_workspace_bytes(M, N, K, ctypes.byref(nbytes)))
+        if ws is None:
+            ws = torch.zeros(nbytes.value, dtype=torch.uint8, device="cuda")
+        native.gemm(a, b, bias=bias, epilogue=native.EPI_F32_BIAS_RESID, out=out, workspace=ws)
+        torch.cuda.synchronize()
+        ref = resid + a.float() @ b.float().t() + bias.float()
+        assert _rel_err(out, ref) < 2e-3
+
+
+def test_layernorm_and_argmax():
+    x = torch.randn(37, 5120, device="cuda") * 3 + 1
+    w = torch.randn(5120, device="cuda").bfloat16()
+    b = torch.randn(5120, device="cuda").bfloat16()
+    y = native.layernorm(x, w, b)
+    ref = torch.nn.functional.layer_norm(x, (5120,), w.float(), b.float(), 1e-5)
+    assert (y.float() - ref).abs().max().item() < 0.05
+    logits = torch.randn(9, 50272, device="cuda")
+    logits[3, 17] = logits[3, 40000] = 100.0  # tie -> first index
+    idx = native.argmax(logits)
+    assert idx.tolist() == logits.argmax(dim=1).tolist()
+    assert idx[3].item() == 17
+
+
+def _pool(n_pages, L, H, D, pt, gen):
+    return (torch.randn(n_pages, L, 2, H, pt, D, device="cuda", generator=gen) * 0.5).bfloat16()
+
+
+def _gather_kv(pool, layer, pages, n_tok, pt):
+    # -> K, V [H, n_tok, D] fp32 for one request
+    ks, vs = [], []
+    for p in pages:
+        ks.append(pool[p, layer, 0])
+        vs.append(pool[p, layer, 1])
+    K = torch.cat(ks, dim=1)[:, :n_tok].float()
+    V = torch.cat(vs, dim=1)[:, :n_tok].float()
+    return K, V
+
+
+@pytest.mark.parametrize("ctxs", [[1], [16, 17, 300], [1000, 4097, 40, 2048, 9000]])
+def test_paged_decode_attention(ctxs):
+    g = torch.Generator(device="cuda").manual_seed(len(ctxs))
+    L, H, D, pt = 3, 8, 128, 16
+    n_pages = sum((c + pt - 1) // pt for c in ctxs) + 4
+    pool = _pool(n_pages, L, H, D, pt, g)
+    perm = torch.randperm(n_pages, generator=torch.Generator().manual_seed(0)).tolist()
+    stride = max((c + pt - 1) // pt for c in ctxs)
+    bt = torch.zeros(len(ctxs), stride, dtype=torch.int32)
+    cur = 0
+    tables = []
+    for b, c in enumerate(ctxs):
+        np_ = (c + pt - 1) // pt
+        pages = perm[cur:cur + np_]
+        cur += np_
+        bt[b, :np_] = torch.tensor(pages, dtype=torch.int32)
+        tables.append(pages)
+    q = torch.randn(len(ctxs), H, D, device="cuda", generator=g).bfloat16()
+    lens = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    layer = 1
+    o = native.paged_decode_attention(q, pool, layer, L, bt.cuda(), lens, pt)
+    torch.cuda.synchronize()
+    for b, c in enumerate(ctxs):
+        K, V = _gather_kv(pool, layer, tables[b], c, pt)
+        s = torch.einsum("hd,htd->ht", q[b].float(), K) * D ** -0.5
+        ref = torch.einsum("ht,htd->hd", torch.softmax(s, dim=-1), V)
+        assert (o[b].float() - ref).abs().max().item() < 2e-2
+
+
+def test_chunk_attention_mixed_slices():
+    """A chunk holding a prompt tail with a long prefix, two whole prompts and a head."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    L, H, D, pt = 2, 4, 128, 16
+    # (prefix already in pages, tokens in this chunk)
+    reqs = [(394, 118), (0, 18), (0, 100), (0, 276)]
+    pages_per = [(s + n + pt - 1) // pt for s, n in reqs]
+    n_pages = sum(pages_per)
+    pool = _pool(n_pages, L, H, D, pt, g)
+    bt, slices, off = [], [], 0
+    for (s, n), np_ in zip(reqs, pages_per):
+        slices.append((s, n, off, np_, 1))
+        bt.extend(range(off, off + np_))
+        off += np_
+    n_tok = sum(n for _, n in reqs)
+    qkv = torch.randn(n_tok, 3 * H * D, device="cuda", generator=g).bfloat16()
+    layer = 1
+    o = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bt, pt)
+    torch.cuda.synchronize()
+    row = 0
+    for (s, n, bto, np_, _) in slices:
+        K, V = _gather_kv(pool, layer, bt[bto:bto + np_], s + n, pt)
+        q = qkv[row:row + n, :H * D].float().view(n, H, D).transpose(0, 1)  # H, n, D
+        sc = torch.einsum("hqd,hkd->hqk", q, K) * D ** -0.5
+        qpos = torch.arange(s, s + n, device="cuda")[:, None]
+        kpos = torch.arange(0, s + n, device="cuda")[None, :]
+        sc = sc.masked_fill(kpos > qpos, float("-inf"))
+        ref = torch.einsum("hqk,hkd->hqd", torch.softmax(sc, -1), V).transpose(0, 1).reshape(n, H * D)
+        err = (o[row:row + n].float() - ref).abs().max().item()
+        assert err < 2e-2, (s, n, err)
+        row += n
