@@ -1,0 +1,169 @@
+"""End-to-end device parity through the C ABI (tk_prefill_chunk,
+tk_decode_step, tk_kv_send, tk_predict) against the fp32 oracle.
+
+Tolerance (bf16 path vs fp32 oracle): logits agree to within 3% of the
+row's logit range (max |diff| <= 0.03 * (max - min) of the oracle row) and
+cosine similarity >= 0.999; greedy tokens must be identical wherever the
+oracle's top-1/top-2 margin exceeds that bound (near-ties are excluded, as
+SURVEY.md §7 prescribes for random weights).  KV handoff is bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.model_ref import ARCH_LLAMA, ARCH_OPT, OracleModel, PagedCache, Shape, bf16_bits_to_f32
+from paper_2401_11181_b200 import native
+from paper_2401_11181_b200.prefill import chunkify
+from paper_2401_11181_b200.workload import Request, token_ids_for
+
+pytestmark = pytest.mark.gpu
+
+PT = 16
+
+
+def _oshape(m: native.ModelShape) -> Shape:
+    return Shape(m.arch, m.n_layers, m.hidden, m.n_heads, m.ffn, m.vocab, m.max_positions,
+                 m.n_labels, m.norm_eps, m.rope_theta)
+
+
+def _close(got: torch.Tensor, ref: torch.Tensor):
+    span = (ref.max(-1).values - ref.min(-1).values).clamp_min(1e-6)
+    err = ((got - ref).abs().max(-1).values / span).max().item()
+    cos = torch.nn.functional.cosine_similarity(got, ref, dim=-1).min().item()
+    assert err <= 0.03 and cos >= 0.999, (err, cos)
+    return err
+
+
+def _greedy_agrees(got: torch.Tensor, ref: torch.Tensor):
+    top2 = ref.topk(2, dim=-1)
+    span = ref.max(-1).values - ref.min(-1).values
+    decided = (top2.values[:, 0] - top2.values[:, 1]) > 0.03 * span
+    assert (got.argmax(-1)[decided] == ref.argmax(-1)[decided]).all()
+    return int(decided.sum())
+
+
+def _plan(lens, chunk_size):
+    reqs = [Request(id=i, arrival_us=0, prompt_len=n, true_decode_len=8) for i, n in enumerate(lens)]
+    tables, nxt = {}, 0
+    for r in reqs:
+        np_ = (r.prompt_len + 8 + PT - 1) // PT
+        tables[r.id] = list(range(nxt, nxt + np_))
+        nxt += np_
+    return reqs, tables, nxt, chunkify(reqs, chunk_size)
+
+
+@pytest.mark.parametrize("model", [native.TINY_OPT, native.TINY_LLAMA])
+def test_prefill_and_decode_match_oracle(model):
+    lens = [18, 100, 512 + 7, 900, 5]
+    reqs, tables, n_pages, chunks = _plan(lens, 512)
+    inst = native.Instance(model, device=0, seed=3, kv_pages=n_pages, page_tokens=PT, max_chunk=512)
+    ora = OracleModel.from_instance(_oshape(model), inst)
+    cache = PagedCache(ora.s, n_pages, PT)
+    prompts = {r.id: token_ids_for(r, model.vocab, seed=11) for r in reqs}
+    first_dev, first_ref = {}, {}
+    for chunk in chunks:
+        ids, slices, bt = [], [], []
+        for rid, start, n in chunk.slices:
+            ids += prompts[rid][start:start + n]
+            slices.append((start, n, len(bt), len(tables[rid]), int(start + n == lens[rid])))
+            bt += tables[rid]
+        ev, toks, logits = inst.prefill_chunk(ids, slices, bt, want_logits=True)
+        ev.wait()
+        ref = ora.prefill_chunk(cache, ids, slices, bt)
+        emitting = [rid for rid, s, n in chunk.slices if s + n == lens[rid]]
+        if emitting:
+            _close(torch.from_numpy(logits), ref)
+            _greedy_agrees(torch.from_numpy(logits), ref)
+            for (rid, s, n), t in zip(chunk.slices, list(toks)):
+                if s + n == lens[rid]:
+                    assert t == int(np.argmax(logits[emitting.index(rid)]))
+        for rid, row_d, row_r in zip(emitting, logits, ref):
+            first_dev[rid], first_ref[rid] = row_d, row_r
+    # KV pages written by the device match the oracle's pages
+    got_page = bf16_bits_to_f32(inst.read_page(tables[2][3])).view(cache.pages[0].shape)
+    assert (got_page - cache.pages[tables[2][3]]).abs().max().item() < 0.05
+    # three decode steps, feeding the oracle's greedy tokens to both sides
+    last = [int(first_ref[i].argmax()) for i in range(len(lens))]
+    ctx = list(lens)
+    stride = max(len(t) for t in tables.values())
+    for _ in range(3):
+        bt = []
+        for i in range(len(lens)):
+            bt += tables[i] + [0] * (stride - len(tables[i]))
+        ev, toks, logits = inst.decode_step(last, ctx, bt, stride, want_logits=True)
+        ev.wait()
+        ref = ora.decode_step(cache, last, ctx, [tables[i] for i in range(len(lens))])
+        _close(torch.from_numpy(logits), ref)
+        _greedy_agrees(torch.from_numpy(logits), ref)
+        assert list(toks) == [int(v) for v in np.argmax(logits, axis=1)]
+        last = [int(v) for v in ref.argmax(-1)]
+        ctx = [c + 1 for c in ctx]
+    inst.close()
+
+
+def test_kv_handoff_bit_exact_and_decode_on_receiver():
+    model = native.TINY_OPT
+    lens = [300, 40]
+    reqs, tables, n_pages, chunks = _plan(lens, 512)
+    p = native.Instance(model, device=0, seed=5, kv_pages=n_pages, max_chunk=512)
+    d = native.Instance(model, device=0, seed=5, kv_pages=n_pages + 7, max_chunk=64)
+    prompts = {r.id: token_ids_for(r, model.vocab, seed=1) for r in reqs}
+    for chunk in chunks:
+        ids, slices, bt = [], [], []
+        for rid, start, n in chunk.slices:
+            ids += prompts[rid][start:start + n]
+            slices.append((start, n, len(bt), len(tables[rid]), int(start + n == lens[rid])))
+            bt += tables[rid]
+        ev, toks = p.prefill_chunk(ids, slices, bt)
+        ev.wait()
+        first = list(toks)
+    # scattered destination pages (reverse order, offset) exercise the page map
+    src = tables[0][: (lens[0] + PT - 1) // PT]
+    dst = [n_pages + 6 - i for i in range(len(src))]
+    ev = d_ev = p.kv_send(src, d, dst)
+    ev.wait()
+    for s_, d_ in zip(src, dst):
+        assert np.array_equal(p.read_page(s_), d.read_page(d_))
+    # decoding on the receiver equals decoding on the sender
+    stride = len(tables[0]) + 1
+    bt_src = tables[0] + [0] * (stride - len(tables[0]))
+    bt_dst = dst + list(range(len(dst), stride))
+    e1, t1, l1 = p.decode_step([first[-1] if first[-1] >= 0 else 5], [lens[0]], bt_src, stride,
+                               want_logits=True)
+    e2, t2, l2 = d.decode_step([first[-1] if first[-1] >= 0 else 5], [lens[0]], bt_dst, stride,
+                               want_logits=True)
+    e1.wait(), e2.wait()
+    assert np.array_equal(l1, l2)
+    assert d_ev.elapsed_ns >= 0
+    p.close(), d.close()
+
+
+def test_predictor_classifier_matches_oracle():
+    model = native.ModelShape("cls-small", native.TK_ARCH_OPT, 2, 768, 12, 3072, 50272,
+                              max_positions=2048, n_labels=41)
+    inst = native.Instance(model, device=0, seed=9, kv_pages=256, max_chunk=2048)
+    ora = OracleModel.from_instance(_oshape(model), inst)
+    lens = [18, 512, 77, 300]
+    g = torch.Generator().manual_seed(0)
+    prompts = [torch.randint(2, model.vocab, (n,), generator=g).tolist() for n in lens]
+    ev, buckets = inst.predict(sum(prompts, []), lens, max_len=512)
+    ev.wait()
+    ref = torch.stack([ora.full_forward(p)[-1] for p in prompts])
+    top2 = ref.topk(2, -1)
+    span = ref.max(-1).values - ref.min(-1).values
+    for i in range(len(lens)):
+        if top2.values[i, 0] - top2.values[i, 1] > 0.03 * span[i]:
+            assert buckets[i] == int(ref[i].argmax())
+    assert all(0 <= b < 41 for b in buckets)
+    inst.close()
+
+
+def test_errors_are_loud():
+    inst = native.Instance(native.TINY_OPT, device=0, kv_pages=4, max_chunk=64)
+    with pytest.raises(ValueError):
+        inst.prefill_chunk([1] * 65, [(0, 65, 0, 4, 1)], [0, 1, 2, 3])
+    from paper_2401_11181_b200.engine import SimulationError
+    with pytest.raises(SimulationError):
+        inst.prefill_chunk([1] * 16, [(0, 16, 0, 1, 1)], [99])
+    inst.close()
