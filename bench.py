@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark of the TetriInfer chunked-prefill data path on B200 (BASELINE.json configs[1]).
+
+Workload (C2): OPT-13B-shaped random-init weights (bf16), 64 prompts drawn
+uniformly from {2048, 4096, 6144, 8192} tokens (synthetic token ids), the
+reference prefill scheduler (SJF, PrefillSchedBatch 16, ChunkSize 512; pdsim
+schedule_round/chunkify) on one prefill instance per GPU.
+
+A *step* is one scheduling round: the 16 prompts of the round chunked at 512
+and run chunk by chunk through the C ABI (tk_prefill_chunk), each chunk
+attending over its requests' accumulated paged KV, first tokens read back for
+the finishing prompts.  Rounds cycle through the workload's 4 rounds.
+
+* ``value``  prefill tokens/s from device time (CUDA events on the compute
+  stream from the first chunk's start to the last chunk's end of each round),
+  whole job over all ranks (max time over ranks).
+* ``e2e``    same tokens over host wall time of the same rounds through the
+  public API with host buffers: ids/slices/page tables staged from pinned host
+  memory each chunk, first tokens read back each chunk.
+* ``roofline`` dominant kernel = the tcgen05 GEMM (QKV/O/FC1/FC2): algorithmic
+  FLOPs / summed CUDA-event durations of its launches in the timed region,
+  against MEASURED_PEAKS.json bf16 sustained (a kernel timed inside a long step).
+* ``cpu_baseline`` the fp32 oracle port (oracle/model_ref.py) on the host cores
+  on a bounded sample (one OPT-13B layer on sampled chunks, x40 layers).
+
+Multi-GPU (torchrun): every rank runs an independent prefill replica of the
+same workload (weak scaling; the prefill path has no data-path collective).
+``--impl reference`` times the CPU port alone (rank 0; other ranks exit 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PROMPT_CHOICES = (2048, 4096, 6144, 8192)
+N_PROMPTS = 64
+CHUNK = 512
+SCHED_BATCH = 16
+PAGE = 16
+METRIC = "prefill tok/s & decode tok/s per GPU; mean TTFT and JCT on mixed workload"
+
+
+def build_workload(seed: int = 0):
+    from paper_2401_11181_b200.engine import RngStreams
+    from paper_2401_11181_b200.prefill import PrefillPolicy, chunkify, schedule_round
+    from paper_2401_11181_b200.workload import Request
+    rng = RngStreams(seed).stream("workload")
+    reqs = [Request(id=i, arrival_us=0, prompt_len=rng.choice(PROMPT_CHOICES), true_decode_len=1)
+            for i in range(N_PROMPTS)]
+    rounds, raw = [], list(reqs)
+    while raw:
+        batch, raw = schedule_round(PrefillPolicy("sjf", SCHED_BATCH), raw)
+        rounds.append((batch, chunkify(batch, CHUNK)))
+    return reqs, rounds
+
+
+def round_plan(batch, chunks, vocab: int, seed: int):
+    """Per chunk: (ids, slices, block_tables, real_tokens); pages laid out per request."""
+    from paper_2401_11181_b200.workload import token_ids_for
+    tables, nxt = {}, 0
+    for r in batch:
+        n = (r.prompt_len + PAGE - 1) // PAGE
+        tables[r.id] = list(range(nxt, nxt + n))
+        nxt += n
+    lens = {r.id: r.prompt_len for r in batch}
+    ids_of = {r.id: token_ids_for(r, vocab, seed) for r in batch}
+    plan = []
+    for c in chunks:
+        ids, slices, bt = [], [], []
+        for rid, start, n in c.slices:
+            ids += ids_of[rid][start:start + n]
+            slices.append((start, n, len(bt), len(tables[rid]), int(start + n == lens[rid])))
+            bt += tables[rid]
+        plan.append((ids, slices, bt, c.real_tokens))
+    return plan, nxt
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows if len(r) >= 8
+                          for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "MEASURED_PEAKS.json"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------- CPU port (oracle)
+
+def cpu_port_sample(plan_chunks, max_seconds: float = 25.0, threads: int | None = None):
+    """fp32 oracle timing of sampled chunks, one OPT-13B layer each (x40 extrapolated).
+
+    plan_chunks: list of (slices, real_tokens).  Returns (tok_s, cores, sample_desc).
+    """
+    import torch
+    from oracle.model_ref import ARCH_OPT, OracleModel, PagedCache, Shape
+    cores = threads or os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    full_layers = 40
+    shape = Shape(ARCH_OPT, n_layers=1, hidden=5120, n_heads=40, ffn=20480, vocab=8,
+                  max_positions=10240)
+    g = torch.Generator().manual_seed(0)
+    h, f = 5120, 20480
+    w = {"embed_tokens.weight": torch.zeros(8, h),
+         "embed_positions.weight": torch.zeros(10242, h),
+         "layers.0.self_attn_layer_norm.weight": torch.ones(h),
+         "layers.0.self_attn_layer_norm.bias": torch.zeros(h),
+         "layers.0.self_attn.qkv_proj.weight": torch.randn(3 * h, h, generator=g) * 0.02,
+         "layers.0.self_attn.qkv_proj.bias": torch.zeros(3 * h),
+         "layers.0.self_attn.out_proj.weight": torch.randn(h, h, generator=g) * 0.02,
+         "layers.0.self_attn.out_proj.bias": torch.zeros(h),
+         "layers.0.final_layer_norm.weight": torch.ones(h),
+         "layers.0.final_layer_norm.bias": torch.zeros(h),
+         "layers.0.fc1.weight": torch.randn(f, h, generator=g) * 0.02,
+         "layers.0.fc1.bias": torch.zeros(f),
+         "layers.0.fc2.weight": torch.randn(h, f, generator=g) * 0.02,
+         "layers.0.fc2.bias": torch.zeros(h)}
+    ora = OracleModel(shape, w)
+    spent, tokens, done = 0.0, 0, 0
+    for slices, real in plan_chunks:
+        top = max(s + n for s, n, *_ in slices)
+        cache = PagedCache(shape, (top + PAGE - 1) // PAGE * len(slices) + 1, PAGE)
+        rows, row, tbl_off = [], 0, 0
+        for s, n, *_ in slices:
+            np_ = (s + n + PAGE - 1) // PAGE
+            table = list(range(tbl_off, tbl_off + np_))
+            tbl_off += np_
+            rows.append((table, torch.arange(s, s + n), slice(row, row + n)))
+            row += n
+        x = torch.randn(real, h, generator=g)
+        t = time.perf_counter()
+        with torch.no_grad():
+            ora.layer(0, x, rows, cache)
+        spent += time.perf_counter() - t
+        tokens += real
+        done += 1
+        if spent * full_layers > 0 and spent > max_seconds:
+            break
+    tok_s = tokens / (spent * full_layers)
+    desc = (f"fp32 torch oracle, {done} sampled C2 chunks ({tokens} tokens), one OPT-13B layer "
+            f"each incl. paged causal attention over the real prefix, x{full_layers} layers")
+    return tok_s, cores, desc
+
+
+# ---------------------------------------------------------------- arms
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def dist_max(value: float, world: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    reqs, rounds = build_workload(args.seed)
+    all_chunks = [(c.slices, c) for _, chs in rounds for c in chs]
+    n = len(all_chunks)
+    total = args.warmup + args.steps
+    idx = [int(i * n / total) for i in range(total)]
+    samples = []
+    for i in idx:
+        batch = [r for r, chs in rounds if all_chunks[i][1] in chs][0]
+        lens = {r.id: r.prompt_len for r in batch}
+        sl = [(s, ln, 0, 0, int(s + ln == lens[rid])) for rid, s, ln in all_chunks[i][1].slices]
+        samples.append((sl, all_chunks[i][1].real_tokens))
+    # warmup steps untimed
+    for s in samples[:args.warmup]:
+        cpu_port_sample([s], max_seconds=1e9)
+    t0 = time.perf_counter()
+    tok_s, cores, desc = cpu_port_sample(samples[args.warmup:], max_seconds=1e9)
+    wall = time.perf_counter() - t0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(tok_s, 3), "unit": "tok/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(wall / max(1, args.steps) * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "C2: OPT-13B-shaped chunked prefill, ChunkSize 512, 64 prompts "
+                               "uniform over 2k/4k/6k/8k, SJF PrefillSchedBatch 16",
+                   "step": "one sampled chunk, one layer x40 (CPU port)"},
+        "cpu_baseline": {"value": round(tok_s, 3), "unit": "tok/s", "cores": cores,
+                         "kind": "port", "sample": desc},
+        "e2e": {"value": round(tok_s, 3), "unit": "tok/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args, world, rank, local):
+    from paper_2401_11181_b200 import native
+    native.load()
+    shape = native.MODELS[args.model]
+    reqs, rounds = build_workload(args.seed)
+    plans, max_pages = [], 0
+    for batch, chunks in rounds:
+        plan, pages = round_plan(batch, chunks, shape.vocab, args.seed)
+        plans.append(plan)
+        max_pages = max(max_pages, pages)
+    inst = native.Instance(shape, device=local, seed=args.seed, kv_pages=max_pages,
+                           page_tokens=PAGE, max_chunk=CHUNK)
+
+    def run_round(plan):
+        evs, toks = [], 0
+        h2d = d2h = 0
+        for ids, slices, bt, real in plan:
+            ev, out = inst.prefill_chunk(ids, slices, bt)
+            a, b = inst.staged_bytes()
+            h2d, d2h = h2d + a, d2h + b
+            evs.append((ev, out))
+            toks += real
+        for ev, _ in evs:
+            ev.wait()  # publishes each chunk's first tokens to host memory
+        dev_ns = native.event_elapsed_ns(evs[0][0], evs[-1][0])
+        return toks, dev_ns, h2d, d2h
+
+    for i in range(args.warmup):
+        run_round(plans[i % len(plans)])
+    inst.sync()
+    clocks = ClockSampler(local)
+    barrier(world)
+    inst.sync()
+    clocks.start()
+    inst.profile(True)
+    launches0 = native.launch_count()
+    t0 = time.perf_counter()
+    tokens = dev_ns = h2d = d2h = 0
+    for i in range(args.steps):
+        t, ns, a, b = run_round(plans[(args.warmup + i) % len(plans)])
+        tokens, dev_ns, h2d, d2h = tokens + t, dev_ns + ns, h2d + a, d2h + b
+    inst.sync()
+    wall = time.perf_counter() - t0
+    launches = native.launch_count() - launches0
+    barrier(world)
+    clk = clocks.stop()
+    prof = inst.profile_read()
+    inst.profile(False)
+
+    dev_s = dist_max(dev_ns / 1e9, world)
+    wall_s = dist_max(wall, world)
+    total_tokens = tokens * world
+    peaks = measured_peaks()
+    gemm_kinds = ("qkv_gemm", "o_gemm", "fc1_gemm", "fc2_gemm")
+    g_ms = sum(prof[k]["ms"] for k in gemm_kinds)
+    g_fl = sum(prof[k]["flops"] for k in gemm_kinds)
+    g_n = sum(prof[k]["launches"] for k in gemm_kinds)
+    achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms else 0.0
+    peak = peaks["bf16_tflops_sustained"]
+    attn = prof["attention"]
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC,
+        "value": round(total_tokens / dev_s, 2),
+        "unit": "tok/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(dev_s / args.steps * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (random-init OPT-13B-shaped weights, synthetic token ids)",
+        "config": {
+            "workload": "C2: OPT-13B-shaped chunked prefill only, ChunkSize 512, 64 prompts "
+                        "uniform over 2k/4k/6k/8k tokens, SJF PrefillSchedBatch 16, 1 prefill "
+                        "instance per GPU",
+            "model": shape.name, "chunk_size": CHUNK, "page_tokens": PAGE,
+            "step": "one scheduling round (16 prompts, all chunks, first tokens read back)",
+            "tokens_per_step": tokens // max(1, args.steps),
+            "parallelism": f"replicas x{world} (weak)",
+            "l2": "inputs larger than L2 (25.8 GB of weights streamed per chunk)",
+        },
+        "e2e": {"value": round(total_tokens / wall_s, 2), "unit": "tok/s",
+                "h2d_bytes_per_step": h2d // max(1, args.steps),
+                "d2h_bytes_per_step": d2h // max(1, args.steps)},
+        "gpu_launches": launches,
+        "roofline": {
+            "kernel": "gemm_tn_kernel (tcgen05 stream-K; QKV/O/FC1/FC2)",
+            "bound": "tensor", "achieved": round(achieved, 2), "peak": peak,
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+            "peak_source": peaks["source"] + " bf16_tflops_sustained",
+            "launches": g_n, "avg_launch_us": round(g_ms * 1e3 / max(1, g_n), 2),
+            "traffic": None,
+        },
+        "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                        "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 2) if v["ms"] and v["flops"] else None,
+                        "gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] else None}
+                    for k, v in prof.items()},
+        "clocks": clk,
+    }
+    line["share_of_step"] = {k: round(v["ms"] / (dev_s * 1e3 / world * world), 4)
+                             for k, v in prof.items()}
+    if world == 1 and not args.no_cpu_baseline:
+        all_chunks = [(p[1], p[3]) for plan in plans for p in plan]
+        pick = [all_chunks[int(i * len(all_chunks) / 6)] for i in range(6)]
+        tok_s, cores, desc = cpu_port_sample(pick, max_seconds=args.cpu_seconds)
+        line["cpu_baseline"] = {"value": round(tok_s, 3), "unit": "tok/s", "cores": cores,
+                                "kind": "port", "sample": desc}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tetri", choices=["tetri", "reference"])
+    ap.add_argument("--model", default="opt-13b")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -147,6 +147,24 @@ int tk_event_query(tk_event* ev, int64_t* elapsed_ns);
 int tk_event_wait(tk_event* ev, int64_t* elapsed_ns);
 int tk_event_release(tk_event* ev);
 int tk_instance_sync(tk_instance* inst);
+/* Device time between the start marker of `a` and the end marker of `b`
+ * (both done; same device).                                                 */
+int tk_event_elapsed(tk_event* a, tk_event* b, int64_t* elapsed_ns);
+
+/* --- instrumentation --------------------------------------------------------
+ * Kernels launched by this library since load (all instances).             */
+int tk_launch_count(int64_t* n);
+/* Bytes the last data-path call on `inst` staged host->device and will copy
+ * device->host (metadata + ids in, tokens out).                             */
+int tk_last_staged_bytes(tk_instance* inst, int64_t* h2d, int64_t* d2h);
+/* Per-kernel-class timing with CUDA events on the launching stream.  Kinds:
+ * 0 QKV GEMM, 1 O GEMM, 2 FC1/gate-up GEMM, 3 FC2/down GEMM, 4 attention,
+ * 5 head (LM/score GEMM), 6 other (norms, embed, KV write, argmax).
+ * tk_profile_read synchronizes, returns the totals since the last read for
+ * one kind (algorithmic FLOPs and bytes as defined in DESIGN.md) and resets. */
+int tk_profile_enable(tk_instance* inst, int32_t on);
+int tk_profile_read(tk_instance* inst, int32_t kind, int64_t* launches, double* total_ms,
+                    double* flops, double* bytes);
 
 /* --- raw kernels on device pointers (parity tests / microbenchmarks) -------
  * C[M,N] = A[M,K] . B[N,K]^T (+ bias[N]) (relu) (+ residual) ; A,B bf16 K-major.

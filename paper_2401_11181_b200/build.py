@@ -63,7 +63,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose and out:
             print(out.decode())
     tmp = LIB.with_suffix(".so.tmp")
-    link = [nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
+    # cudart is linked as a shared library: a statically linked runtime inside
+    # a dlopen()ed library hides its launches from Nsight Compute.
+    link = [nvcc, *ARCH, "-shared", "-cudart", os.environ.get("TK_CUDART", "shared"), "-o",
+            str(tmp), *map(str, objs), "-Xlinker", "-rpath,$ORIGIN"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(link)}\n{r.stdout}{r.stderr}")

@@ -22,9 +22,14 @@
 // wave quantisation of M=512 chunk GEMMs (e.g. 80 tiles of 128x256 at
 // N=5120 on 148 SMs) and of skinny decode GEMMs alike.
 //
-// Tiles are numbered m-fastest so CTAs running concurrently share the same
-// weight panel: each weight byte is read from HBM once per GEMM and served
-// to the other m-tiles from L2.
+// Weight reuse: CTAs are launched in clusters of CS = min(tiles_m, 4) along M.
+// The cluster walks one weight panel in lock step; each CTA TMA-loads 1/CS of
+// every weight tile and multicasts it into all CS CTAs' shared memory, and
+// every CTA's MMA commit releases the stage in all CS CTAs.  Each weight byte
+// is therefore fetched from L2/HBM once per GEMM (not once per m-tile), and
+// each SM pulls 16 KB of A + 32/CS KB of B per k-block.  The stream-K split
+// runs over the cluster-level (m-group, n-tile, k-block) space; the number of
+// clusters comes from cudaOccupancyMaxActiveClusters so all are co-resident.
 #include "tk_common.cuh"
 #include "tk_kernels.h"
 
@@ -46,6 +51,7 @@ struct GemmCfg {
 
 struct GemmArgs {
   void* C;
+  int cs;  // cluster size along M (1, 2 or 4)
   const __nv_bfloat16* bias;
   float* ws;
   int* counters;
@@ -111,7 +117,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& p, int row, int c
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CS>
 __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const GemmArgs p) {
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
     tma_prefetch_desc(&tmap_b);
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CS);  // released by the MMA commit of every CTA of the cluster
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -146,15 +152,22 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
   }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CS > 1) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // cluster-level stream-K partition over (m-group, n-tile, k-block)
+  const int rank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int cluster = blockIdx.x / CS;
+  const int G = gridDim.x / CS;
+  const int groups_m = p.tiles_m / CS;
   const long long T = p.total_iters;
-  const int G = gridDim.x;
-  const long long it_begin = static_cast<long long>(blockIdx.x) * T / G;
-  const long long it_end = static_cast<long long>(blockIdx.x + 1) * T / G;
+  const long long it_begin = static_cast<long long>(cluster) * T / G;
+  const long long it_end = static_cast<long long>(cluster + 1) * T / G;
   const int kbs = p.kbs;
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CS) - 1);
+  constexpr int B_SLICE_ROWS = BN / CS;
+  constexpr int B_SLICE_BYTES = B_SLICE_ROWS * Cfg::BK * 2;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -164,18 +177,24 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (long long i = it_begin; i < it_end;) {
-        const int tile = static_cast<int>(i / kbs);
-        const long long seg_end = min(it_end, static_cast<long long>(tile + 1) * kbs);
-        const int m_idx = tile % p.tiles_m;
-        const int n_idx = tile / p.tiles_m;
-        for (int kb = static_cast<int>(i - static_cast<long long>(tile) * kbs);
-             kb < static_cast<int>(seg_end - static_cast<long long>(tile) * kbs); ++kb) {
+        const int ctile = static_cast<int>(i / kbs);
+        const long long seg_end = min(it_end, static_cast<long long>(ctile + 1) * kbs);
+        const int m_idx = (ctile % groups_m) * CS + rank;
+        const int n_idx = ctile / groups_m;
+        for (int kb = static_cast<int>(i - static_cast<long long>(ctile) * kbs);
+             kb < static_cast<int>(seg_end - static_cast<long long>(ctile) * kbs); ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           tma_load_2d(sa + stage * Cfg::A_BYTES, &tmap_a, &full[stage], kb * Cfg::BK,
                       m_idx * Cfg::BM, pol_a);
-          tma_load_2d(sb + stage * Cfg::B_BYTES, &tmap_b, &full[stage], kb * Cfg::BK,
-                      n_idx * BN, pol_b);
+          if constexpr (CS == 1) {
+            tma_load_2d(sb + stage * Cfg::B_BYTES, &tmap_b, &full[stage], kb * Cfg::BK,
+                        n_idx * BN, pol_b);
+          } else {
+            tma_load_2d_mc(sb + stage * Cfg::B_BYTES + rank * B_SLICE_BYTES, &tmap_b,
+                           &full[stage], kb * Cfg::BK, n_idx * BN + rank * B_SLICE_ROWS, kMask,
+                           pol_b);
+          }
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -193,8 +212,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (long long i = it_begin; i < it_end;) {
-        const int tile = static_cast<int>(i / kbs);
-        const long long seg_end = min(it_end, static_cast<long long>(tile + 1) * kbs);
+        const int ctile = static_cast<int>(i / kbs);
+        const long long seg_end = min(it_end, static_cast<long long>(ctile + 1) * kbs);
         const int nkb = static_cast<int>(seg_end - i);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -209,7 +228,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
             umma_bf16(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
                       idesc, (k > 0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (CS == 1) umma_commit(&empty[stage]);
+          else umma_commit_mc(&empty[stage], kMask);
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -229,11 +249,12 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (long long i = it_begin; i < it_end;) {
-      const int tile = static_cast<int>(i / kbs);
-      const long long tile_first = static_cast<long long>(tile) * kbs;
+      const int ctile = static_cast<int>(i / kbs);
+      const long long tile_first = static_cast<long long>(ctile) * kbs;
       const long long seg_end = min(it_end, tile_first + kbs);
-      const int m_idx = tile % p.tiles_m;
-      const int n_idx = tile / p.tiles_m;
+      const int m_idx = (ctile % groups_m) * CS + rank;
+      const int n_idx = ctile / groups_m;
+      const int tile = n_idx * p.tiles_m + m_idx;
       const int row = m_idx * Cfg::BM + row_in_tile;
       const int col_base = n_idx * BN;
       const int contrib = owner_of(tile_first + kbs - 1, T, G) - owner_of(tile_first, T, G) + 1;
@@ -263,6 +284,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
           uint32_t r[32];
           tmem_ld_32x32b_x32(t_row + c * 32, r);
           tmem_wait_ld();
+          if (row >= p.M) continue;  // rows past M are zero (TMA zero-fill)
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             atomicAdd(reinterpret_cast<float4*>(ws_row + c * 32 + g * 4),
@@ -280,7 +302,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
           *last_flag = (prev == contrib - 1) ? 1 : 0;
         }
         named_bar_sync(1, 128);
-        if (*last_flag) {
+        if (*last_flag && row < p.M) {
           __threadfence();
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
@@ -294,6 +316,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
             }
             epilogue_store<EPI>(p, row, col_base + c * 32, v);
           }
+        }
+        if (*last_flag) {
           named_bar_sync(1, 128);
           if (leader) atomicExch(p.counters + tile, 0);
         }
@@ -305,7 +329,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  // no CTA may leave while a peer can still multicast into it / arrive on it
+  if constexpr (CS > 1) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
@@ -355,33 +380,81 @@ int64_t gemm_workspace_bytes(int M, int N, int K) {
   return tiles * 128 * bn * 4 + tiles * 4 + 256;
 }
 
-template <int BN, int EPI>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int grid,
-                       cudaStream_t stream) {
+template <int BN, int EPI, int CS>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                       int max_ctas, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
-  static bool configured = false;
-  if (!configured) {
-    TK_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<BN, EPI>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    configured = true;
+  auto kern = gemm_tn_kernel<BN, EPI, CS>;
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM_BYTES));
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(kNumSMs / CS * CS);
+    q.blockDim = dim3(Cfg::THREADS);
+    q.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = CS;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int n = 0;
+    if (CS > 1) {
+      TK_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &q));
+    } else {
+      n = kNumSMs;
+    }
+    max_clusters = n > 0 ? n : 1;
   }
-  gemm_tn_kernel<BN, EPI><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ta, tb, a);
-  TK_CUDA(cudaGetLastError());
+  // clusters: all co-resident, never more than the cluster-level iterations / 4
+  const long long iters = a.total_iters;
+  int clusters = max_clusters;
+  if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / CS));
+  clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, iters / 4)));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * CS);
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
+  note_launch();
   return TK_OK;
 }
 
-template <int BN>
-static int dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int grid,
-                        cudaStream_t s) {
+template <int BN, int CS>
+static int dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                        int max_ctas, cudaStream_t s) {
   switch (a.epi) {
-    case EPI_BF16: return launch_gemm<BN, EPI_BF16>(ta, tb, a, grid, s);
-    case EPI_BF16_BIAS: return launch_gemm<BN, EPI_BF16_BIAS>(ta, tb, a, grid, s);
-    case EPI_BF16_BIAS_RELU: return launch_gemm<BN, EPI_BF16_BIAS_RELU>(ta, tb, a, grid, s);
-    case EPI_F32_BIAS_RESID: return launch_gemm<BN, EPI_F32_BIAS_RESID>(ta, tb, a, grid, s);
-    case EPI_F32: return launch_gemm<BN, EPI_F32>(ta, tb, a, grid, s);
+    case EPI_BF16: return launch_gemm<BN, EPI_BF16, CS>(ta, tb, a, max_ctas, s);
+    case EPI_BF16_BIAS: return launch_gemm<BN, EPI_BF16_BIAS, CS>(ta, tb, a, max_ctas, s);
+    case EPI_BF16_BIAS_RELU: return launch_gemm<BN, EPI_BF16_BIAS_RELU, CS>(ta, tb, a, max_ctas, s);
+    case EPI_F32_BIAS_RESID: return launch_gemm<BN, EPI_F32_BIAS_RESID, CS>(ta, tb, a, max_ctas, s);
+    case EPI_F32: return launch_gemm<BN, EPI_F32, CS>(ta, tb, a, max_ctas, s);
   }
   set_error("unknown gemm epilogue");
   return TK_EINVAL;
+}
+
+template <int BN>
+static int dispatch_cs(const void* B, int N, int K, const CUtensorMap& ta, GemmArgs& a,
+                       int max_ctas, cudaStream_t s) {
+  CUtensorMap tb;
+  int rc = make_tmap_kmajor(&tb, B, N, K, BN / a.cs);
+  if (rc) return rc;
+  switch (a.cs) {
+    case 4: return dispatch_epi<BN, 4>(ta, tb, a, max_ctas, s);
+    case 2: return dispatch_epi<BN, 2>(ta, tb, a, max_ctas, s);
+    default: return dispatch_epi<BN, 1>(ta, tb, a, max_ctas, s);
+  }
 }
 
 int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, int N, int K,
@@ -391,10 +464,8 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   TK_CHECK(N % 8 == 0, TK_EINVAL, "gemm: N must be a multiple of 8");
   TK_CHECK(ws_bytes >= gemm_workspace_bytes(M, N, K), TK_EINVAL, "gemm: workspace too small");
   const int bn = pick_bn(N);
-  CUtensorMap ta, tb;
+  CUtensorMap ta;
   int rc = make_tmap_kmajor(&ta, A, M, K, 128);
-  if (rc) return rc;
-  rc = make_tmap_kmajor(&tb, B, N, K, bn);
   if (rc) return rc;
   GemmArgs a;
   a.C = C;
@@ -406,16 +477,13 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   a.tiles_m = (M + 127) / 128;
   a.tiles_n = (N + bn - 1) / bn;
   a.kbs = K / 64;
+  a.cs = a.tiles_m % 4 == 0 ? 4 : (a.tiles_m % 2 == 0 ? 2 : 1);
   const int64_t tiles = static_cast<int64_t>(a.tiles_m) * a.tiles_n;
-  a.total_iters = tiles * a.kbs;
+  a.total_iters = static_cast<int64_t>(a.tiles_m / a.cs) * a.tiles_n * a.kbs;
   a.ws = static_cast<float*>(workspace);
   a.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(workspace) + tiles * 128 * bn * 4);
-  // Enough k-blocks per CTA to amortise the prologue; never more CTAs than SMs.
-  int grid = static_cast<int>(std::min<int64_t>(max_ctas > 0 ? max_ctas : kNumSMs,
-                                                std::max<int64_t>(1, a.total_iters / 4)));
-  if (tiles >= grid && tiles % grid == 0) grid = static_cast<int>(std::min<int64_t>(grid, tiles));
-  if (bn == 256) return dispatch_epi<256>(ta, tb, a, grid, stream);
-  return dispatch_epi<128>(ta, tb, a, grid, stream);
+  if (bn == 256) return dispatch_cs<256>(B, N, K, ta, a, max_ctas, stream);
+  return dispatch_cs<128>(B, N, K, ta, a, max_ctas, stream);
 }
 
 }  // namespace tk

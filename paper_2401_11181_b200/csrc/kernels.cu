@@ -51,6 +51,7 @@ int launch_embed_opt(const int32_t* ids, const TokenMeta* meta, int n, const __n
   if (n == 0) return TK_OK;
   embed_opt_kernel<<<n, 128, 0, s>>>(ids, meta, tok_emb, pos_emb, resid, hidden);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -68,6 +69,7 @@ int launch_embed_llama(const int32_t* ids, int n, const __nv_bfloat16* tok_emb, 
   if (n == 0) return TK_OK;
   embed_plain_kernel<<<n, 256, 0, s>>>(ids, tok_emb, resid, hidden);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -136,6 +138,7 @@ int launch_layernorm(const float* x, const __nv_bfloat16* w, const __nv_bfloat16
   if (rows == 0) return TK_OK;
   norm_kernel<false><<<rows, kNormThreads, 0, s>>>(x, w, b, y, cols, eps);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -146,6 +149,7 @@ int launch_rmsnorm(const float* x, const __nv_bfloat16* w, __nv_bfloat16* y, int
   if (rows == 0) return TK_OK;
   norm_kernel<true><<<rows, kNormThreads, 0, s>>>(x, w, nullptr, y, cols, eps);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -162,6 +166,7 @@ int launch_gather_rows_f32(const float* x, const int32_t* rows, int n, int cols,
   if (n == 0) return TK_OK;
   gather_rows_kernel<<<n, 256, 0, s>>>(x, rows, cols, out);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -215,6 +220,7 @@ int launch_kv_write(__nv_bfloat16* qkv, const TokenMeta* meta, int n, __nv_bfloa
   if (n == 0) return TK_OK;
   kv_write_kernel<<<n, 256, 0, s>>>(qkv, meta, pool, g, layer, q_scale, rope, rope_theta);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -490,6 +496,7 @@ int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloa
                                                   bt_dev, scale_log2);
   }
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -661,10 +668,12 @@ int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16*
       q, q_stride, o, pool, g, layer, block_tables, bt_stride, ctx_lens, scale_log2,
       static_cast<float*>(workspace), splits);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   if (splits > 1) {
     decode_combine_kernel<128><<<dim3(g.n_heads, batch), 128, 0, s>>>(
         o, g.n_heads, ctx_lens, static_cast<const float*>(workspace), splits);
     TK_CUDA(cudaGetLastError());
+  note_launch();
   }
   return TK_OK;
 }
@@ -715,6 +724,7 @@ int launch_argmax_strided(const float* logits, int rows, int cols, int stride, i
   if (rows == 0) return TK_OK;
   argmax_kernel<<<rows, 1024, 0, s>>>(logits, cols, stride, out);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -744,6 +754,7 @@ int launch_init_normal(__nv_bfloat16* w, int64_t n, uint64_t seed, float std, cu
   if (n == 0) return TK_OK;
   init_normal_kernel<<<kNumSMs * 8, 256, 0, s>>>(w, n, seed, std);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -758,6 +769,7 @@ int launch_fill(__nv_bfloat16* w, int64_t n, float value, cudaStream_t s) {
   if (n == 0) return TK_OK;
   fill_kernel<<<kNumSMs * 4, 256, 0, s>>>(w, n, value);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 
@@ -777,6 +789,7 @@ int launch_swiglu(const __nv_bfloat16* gate_up, __nv_bfloat16* out, int n, int f
   if (n == 0) return TK_OK;
   swiglu_kernel<<<n, 256, 0, s>>>(gate_up, out, ffn);
   TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 

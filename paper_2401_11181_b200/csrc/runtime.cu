@@ -9,6 +9,7 @@
 // single H2D copy.  Every data-path call is asynchronous and returns a
 // tk_event whose completion also publishes the call's small host outputs.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -24,6 +25,9 @@
 namespace tk {
 
 static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_err = msg; }
 
@@ -277,6 +281,16 @@ struct tk_instance {
   int dec_max_ctx = 0;
   tk::Slot ring[tk::kRingSlots];
   int ring_next = 0;
+  int64_t last_h2d = 0, last_d2h = 0;
+  // profiling (tk_profile_*)
+  bool prof = false;
+  struct ProfRec {
+    int kind;
+    double flops, bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> ev_pool;
 };
 
 namespace tk {
@@ -345,49 +359,91 @@ struct Packer {
 
 static float attn_scale(const tk_model_desc& m) { return 1.f / sqrtf(static_cast<float>(m.head_dim)); }
 
+enum ProfKind { PK_QKV = 0, PK_O = 1, PK_FC1 = 2, PK_FC2 = 3, PK_ATTN = 4, PK_HEAD = 5, PK_OTHER = 6 };
+
+static cudaEvent_t pool_event(tk_instance* inst) {
+  if (!inst->ev_pool.empty()) {
+    cudaEvent_t e = inst->ev_pool.back();
+    inst->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Run `op` bracketed by CUDA events on `s` when profiling is on.
+template <typename Op>
+static int profiled(tk_instance* inst, cudaStream_t s, int kind, double flops, double bytes,
+                    Op&& op) {
+  if (!inst->prof) return op();
+  cudaEvent_t a = pool_event(inst), b = pool_event(inst);
+  TK_CUDA(cudaEventRecord(a, s));
+  int rc = op();
+  TK_CUDA(cudaEventRecord(b, s));
+  inst->recs.push_back({kind, flops, bytes, a, b});
+  return rc;
+}
+
 // One transformer layer over `n` rows whose metadata lives on the device.
-// attention_fn performs the attention step writing inst->attn.
+// attention_fn performs the attention step writing inst->attn; attn_flops /
+// attn_bytes are its algorithmic work.
 template <typename AttnFn>
 static int run_layer(tk_instance* inst, int layer, int n, const TokenMeta* meta_dev,
-                     cudaStream_t s, AttnFn&& attention_fn) {
+                     cudaStream_t s, double attn_flops, double attn_bytes, AttnFn&& attention_fn) {
   const tk_model_desc& m = inst->w->md;
   const LayerW& L = inst->w->layers[layer];
-  const int h = m.hidden;
+  const double h = m.hidden, f = m.ffn, nn = n;
   const bool opt = m.arch == TK_ARCH_OPT;
+  const int hi = m.hidden;
   int rc;
-  rc = opt ? launch_layernorm(inst->resid, L.ln1_w, L.ln1_b, inst->xn, n, h, m.norm_eps, s)
-           : launch_rmsnorm(inst->resid, L.ln1_w, inst->xn, n, h, m.norm_eps, s);
+  rc = profiled(inst, s, PK_OTHER, 0, nn * h * 6, [&] {
+    return opt ? launch_layernorm(inst->resid, L.ln1_w, L.ln1_b, inst->xn, n, hi, m.norm_eps, s)
+               : launch_rmsnorm(inst->resid, L.ln1_w, inst->xn, n, hi, m.norm_eps, s);
+  });
   if (rc) return rc;
-  rc = gemm_bf16(inst->xn, L.qkv_w, inst->qkv, L.qkv_b, n, 3 * h, h,
-                 opt ? EPI_BF16_BIAS : EPI_BF16, inst->gemm_ws, inst->gemm_ws_bytes, s);
+  rc = profiled(inst, s, PK_QKV, 2 * nn * 3 * h * h, (3 * h * h + nn * 4 * h) * 2, [&] {
+    return gemm_bf16(inst->xn, L.qkv_w, inst->qkv, L.qkv_b, n, 3 * hi, hi,
+                     opt ? EPI_BF16_BIAS : EPI_BF16, inst->gemm_ws, inst->gemm_ws_bytes, s);
+  });
   if (rc) return rc;
-  rc = launch_kv_write(inst->qkv, meta_dev, n, inst->pool, inst->geom, layer, 1.f, opt ? 0 : 1,
-                       m.rope_theta, s);
+  rc = profiled(inst, s, PK_OTHER, 0, nn * h * 8, [&] {
+    return launch_kv_write(inst->qkv, meta_dev, n, inst->pool, inst->geom, layer, 1.f,
+                           opt ? 0 : 1, m.rope_theta, s);
+  });
   if (rc) return rc;
-  rc = attention_fn();
+  rc = profiled(inst, s, PK_ATTN, attn_flops, attn_bytes, attention_fn);
   if (rc) return rc;
-  rc = gemm_bf16(inst->attn, L.o_w, inst->resid, L.o_b, n, h, h, EPI_F32_BIAS_RESID,
-                 inst->gemm_ws, inst->gemm_ws_bytes, s);
+  rc = profiled(inst, s, PK_O, 2 * nn * h * h, (h * h + nn * h) * 2 + nn * h * 8, [&] {
+    return gemm_bf16(inst->attn, L.o_w, inst->resid, L.o_b, n, hi, hi, EPI_F32_BIAS_RESID,
+                     inst->gemm_ws, inst->gemm_ws_bytes, s);
+  });
   if (rc) return rc;
-  rc = opt ? launch_layernorm(inst->resid, L.ln2_w, L.ln2_b, inst->xn, n, h, m.norm_eps, s)
-           : launch_rmsnorm(inst->resid, L.ln2_w, inst->xn, n, h, m.norm_eps, s);
+  rc = profiled(inst, s, PK_OTHER, 0, nn * h * 6, [&] {
+    return opt ? launch_layernorm(inst->resid, L.ln2_w, L.ln2_b, inst->xn, n, hi, m.norm_eps, s)
+               : launch_rmsnorm(inst->resid, L.ln2_w, inst->xn, n, hi, m.norm_eps, s);
+  });
   if (rc) return rc;
-  if (opt) {
-    rc = gemm_bf16(inst->xn, L.fc1_w, inst->ffn, L.fc1_b, n, m.ffn, h, EPI_BF16_BIAS_RELU,
-                   inst->gemm_ws, inst->gemm_ws_bytes, s);
-    if (rc) return rc;
-  } else {
-    // gate_up into qkv scratch (2*ffn <= 3*h is not guaranteed: use ffn scratch twice)
-    rc = gemm_bf16(inst->xn, L.fc1_w, inst->ffn, nullptr, n, 2 * m.ffn, h, EPI_BF16,
-                   inst->gemm_ws, inst->gemm_ws_bytes, s);
-    if (rc) return rc;
-    rc = launch_swiglu(inst->ffn, inst->ffn + static_cast<size_t>(n) * 2 * m.ffn, n, m.ffn, s);
+  const double up = opt ? f : 2 * f;
+  rc = profiled(inst, s, PK_FC1, 2 * nn * up * h, (up * h + nn * h + nn * up) * 2, [&] {
+    return opt ? gemm_bf16(inst->xn, L.fc1_w, inst->ffn, L.fc1_b, n, m.ffn, hi, EPI_BF16_BIAS_RELU,
+                           inst->gemm_ws, inst->gemm_ws_bytes, s)
+               : gemm_bf16(inst->xn, L.fc1_w, inst->ffn, nullptr, n, 2 * m.ffn, hi, EPI_BF16,
+                           inst->gemm_ws, inst->gemm_ws_bytes, s);
+  });
+  if (rc) return rc;
+  if (!opt) {
+    rc = profiled(inst, s, PK_OTHER, 0, nn * f * 6, [&] {
+      return launch_swiglu(inst->ffn, inst->ffn + static_cast<size_t>(n) * 2 * m.ffn, n, m.ffn, s);
+    });
     if (rc) return rc;
   }
   const __nv_bfloat16* ffn_act =
       opt ? inst->ffn : inst->ffn + static_cast<size_t>(n) * 2 * m.ffn;
-  rc = gemm_bf16(ffn_act, L.fc2_w, inst->resid, L.fc2_b, n, h, m.ffn, EPI_F32_BIAS_RESID,
-                 inst->gemm_ws, inst->gemm_ws_bytes, s);
+  rc = profiled(inst, s, PK_FC2, 2 * nn * h * f, (h * f + nn * f) * 2 + nn * h * 8, [&] {
+    return gemm_bf16(ffn_act, L.fc2_w, inst->resid, L.fc2_b, n, hi, m.ffn, EPI_F32_BIAS_RESID,
+                     inst->gemm_ws, inst->gemm_ws_bytes, s);
+  });
   return rc;
 }
 
@@ -404,8 +460,13 @@ static int run_head(tk_instance* inst, int n_rows, const int32_t* rows_dev, int3
            ? launch_layernorm(gathered, w->fln_w, w->fln_b, inst->xn, n_rows, m.hidden, m.norm_eps, s)
            : launch_rmsnorm(gathered, w->fln_w, inst->xn, n_rows, m.hidden, m.norm_eps, s);
   if (rc) return rc;
-  rc = gemm_bf16(inst->xn, w->head, inst->logits, nullptr, n_rows, w->head_rows, m.hidden, EPI_F32,
-                 inst->gemm_ws, inst->gemm_ws_bytes, s);
+  rc = profiled(inst, s, PK_HEAD, 2.0 * n_rows * w->head_rows * m.hidden,
+                (static_cast<double>(w->head_rows) * m.hidden + n_rows * m.hidden) * 2 +
+                    static_cast<double>(n_rows) * w->head_rows * 4,
+                [&] {
+                  return gemm_bf16(inst->xn, w->head, inst->logits, nullptr, n_rows, w->head_rows,
+                                   m.hidden, EPI_F32, inst->gemm_ws, inst->gemm_ws_bytes, s);
+                });
   if (rc) return rc;
   const int cols = m.n_labels > 0 ? m.n_labels : m.vocab;
   return launch_argmax_strided(inst->logits, n_rows, cols, w->head_rows, tokens_dev, s);
@@ -644,14 +705,22 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
   rc = new_event(inst, s, &ev);
   if (rc) return rc;
   TK_CUDA(cudaMemcpyAsync(slot->dev, slot->host, pk.off, cudaMemcpyHostToDevice, s));
+  inst->last_h2d = pk.off;
+  inst->last_d2h = static_cast<int64_t>(n_emit) * 4;
   const int h = m.hidden;
   rc = m.arch == TK_ARCH_OPT
            ? launch_embed_opt(ids_d, meta_d, n_tokens, inst->w->embed, inst->w->pos, inst->resid, h, s)
            : launch_embed_llama(ids_d, n_tokens, inst->w->embed, inst->resid, h, s);
   if (rc) return rc;
   const float scale = attn_scale(m);
+  double ctx_sum = 0;  // sum over query rows of keys attended (pos + 1)
+  for (int t = 0; t < n_tokens; ++t) ctx_sum += meta[t].pos + 1;
+  const double attn_flops = 4.0 * m.head_dim * m.n_heads * ctx_sum;
+  int64_t prefix_tokens = 0;
+  for (int i = 0; i < n_slices; ++i) prefix_tokens += slices[i].start + slices[i].len;
+  const double attn_bytes = 2.0 * m.hidden * 2 * prefix_tokens + 2.0 * n_tokens * m.hidden * 2;
   for (int l = 0; l < m.n_layers; ++l) {
-    rc = run_layer(inst, l, n_tokens, meta_d, s, [&]() {
+    rc = run_layer(inst, l, n_tokens, meta_d, s, attn_flops, attn_bytes, [&]() {
       return launch_chunk_attention_work(inst->qkv, 3 * h, inst->attn, inst->pool, inst->geom, l,
                                          work_d, n_work, sl_d, bt_d, scale, s);
     });
@@ -747,14 +816,21 @@ int tk_decode_step(tk_instance* inst, int32_t batch, const int32_t* last_tokens,
   rc = new_event(inst, s, &ev);
   if (rc) return rc;
   TK_CUDA(cudaMemcpyAsync(slot->dev, slot->host, pk.off, cudaMemcpyHostToDevice, s));
+  inst->last_h2d = pk.off;
+  inst->last_d2h = static_cast<int64_t>(batch) * 4;
   const int h = m.hidden;
   rc = m.arch == TK_ARCH_OPT
            ? launch_embed_opt(ids_d, meta_d, batch, inst->w->embed, inst->w->pos, inst->resid, h, s)
            : launch_embed_llama(ids_d, batch, inst->w->embed, inst->resid, h, s);
   if (rc) return rc;
   const float scale = attn_scale(m);
+  double kv_sum = 0;
+  for (int b = 0; b < batch; ++b) kv_sum += ctx_lens[b] + 1;
+  const double attn_flops = 4.0 * m.head_dim * m.n_heads * kv_sum;
+  // K and V of every attended token read once, Q read, O written (one layer)
+  const double attn_bytes = kv_sum * 2.0 * m.hidden * 2 + 2.0 * batch * m.hidden * 2;
   for (int l = 0; l < m.n_layers; ++l) {
-    rc = run_layer(inst, l, batch, meta_d, s, [&]() {
+    rc = run_layer(inst, l, batch, meta_d, s, attn_flops, attn_bytes, [&]() {
       return launch_decode_attention(inst->qkv, 3 * h, inst->attn, inst->pool, inst->geom, l, bt_d,
                                      bt_stride, lens_d, batch, max_ctx, scale, inst->dec_ws,
                                      inst->dec_ws_bytes, s);
@@ -1029,6 +1105,59 @@ int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_
   cudaFree(d_bt);
   cudaFree(d_work);
   return rc;
+}
+
+int tk_event_elapsed(tk_event* a, tk_event* b, int64_t* elapsed_ns) {
+  TK_CHECK(a && b && elapsed_ns, TK_EINVAL, "tk_event_elapsed: null argument");
+  float ms = 0.f;
+  TK_CUDA(cudaEventElapsedTime(&ms, a->start, b->end));
+  *elapsed_ns = static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+  return TK_OK;
+}
+
+int tk_launch_count(int64_t* n) {
+  TK_CHECK(n, TK_EINVAL, "null");
+  *n = g_launches.load();
+  return TK_OK;
+}
+
+int tk_last_staged_bytes(tk_instance* inst, int64_t* h2d, int64_t* d2h) {
+  TK_CHECK(inst && h2d && d2h, TK_EINVAL, "null");
+  *h2d = inst->last_h2d;
+  *d2h = inst->last_d2h;
+  return TK_OK;
+}
+
+int tk_profile_enable(tk_instance* inst, int32_t on) {
+  TK_CHECK(inst, TK_EINVAL, "null instance");
+  inst->prof = on != 0;
+  return TK_OK;
+}
+
+int tk_profile_read(tk_instance* inst, int32_t kind, int64_t* launches, double* total_ms,
+                    double* flops, double* bytes) {
+  TK_CHECK(inst && launches && total_ms && flops && bytes, TK_EINVAL, "null argument");
+  TK_CUDA(cudaSetDevice(inst->device));
+  TK_CUDA(cudaDeviceSynchronize());
+  *launches = 0;
+  *total_ms = *flops = *bytes = 0;
+  std::vector<tk_instance::ProfRec> keep;
+  for (auto& r : inst->recs) {
+    if (r.kind != kind) {
+      keep.push_back(r);
+      continue;
+    }
+    float ms = 0.f;
+    TK_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    *launches += 1;
+    *total_ms += ms;
+    *flops += r.flops;
+    *bytes += r.bytes;
+    inst->ev_pool.push_back(r.a);
+    inst->ev_pool.push_back(r.b);
+  }
+  inst->recs.swap(keep);
+  return TK_OK;
 }
 
 }  // extern "C"

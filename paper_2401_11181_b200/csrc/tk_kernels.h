@@ -10,6 +10,9 @@
 
 namespace tk {
 
+// Count of kernels launched by the library (tk_launch_count).
+void note_launch();
+
 enum Epi : int {
   EPI_BF16 = 0,            // C bf16 = acc
   EPI_BF16_BIAS = 1,       // C bf16 = acc + bias

@@ -68,6 +68,12 @@ _SIGNATURES = {
     "tk_event_wait": ([_P, _I64P], C.c_int),
     "tk_event_release": ([_P], C.c_int),
     "tk_instance_sync": ([_P], C.c_int),
+    "tk_event_elapsed": ([_P, _P, _I64P], C.c_int),
+    "tk_launch_count": ([_I64P], C.c_int),
+    "tk_last_staged_bytes": ([_P, _I64P, _I64P], C.c_int),
+    "tk_profile_enable": ([_P, C.c_int32], C.c_int),
+    "tk_profile_read": ([_P, C.c_int32, _I64P, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                         C.POINTER(C.c_double)], C.c_int),
     "tk_gemm_bf16": ([_P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64,
                       _P], C.c_int),
     "tk_gemm_workspace_bytes": ([C.c_int32, C.c_int32, C.c_int32, _I64P], C.c_int),
@@ -341,6 +347,44 @@ class Instance:
 
     def sync(self) -> None:
         check(load().tk_instance_sync(self._h), "tk_instance_sync")
+
+    # -- instrumentation ----------------------------------------------------------------
+    def staged_bytes(self) -> tuple[int, int]:
+        a, b = C.c_int64(), C.c_int64()
+        check(load().tk_last_staged_bytes(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def profile(self, on: bool) -> None:
+        check(load().tk_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        """Per kernel class: launches, ms, algorithmic flops and bytes (resets)."""
+        out = {}
+        for kind, name in enumerate(PROFILE_KINDS):
+            n, ms, fl, by = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            check(load().tk_profile_read(self._h, kind, C.byref(n), C.byref(ms), C.byref(fl),
+                                         C.byref(by)), "tk_profile_read")
+            out[name] = {"launches": n.value, "ms": ms.value, "flops": fl.value,
+                         "bytes": by.value}
+        return out
+
+
+PROFILE_KINDS = ("qkv_gemm", "o_gemm", "fc1_gemm", "fc2_gemm", "attention", "head_gemm", "other")
+
+
+def event_elapsed_ns(first: Event, last: Event) -> int:
+    """Device time from first's start marker to last's end marker."""
+    first.wait()
+    last.wait()
+    ns = C.c_int64()
+    check(load().tk_event_elapsed(first._ptr, last._ptr, C.byref(ns)), "tk_event_elapsed")
+    return ns.value
+
+
+def launch_count() -> int:
+    n = C.c_int64()
+    check(load().tk_launch_count(C.byref(n)))
+    return n.value
 
 
 def host_alloc(nbytes: int) -> int:

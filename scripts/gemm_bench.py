@@ -1,0 +1,67 @@
+"""Microbenchmark of the tcgen05 GEMM at the OPT-13B chunk shapes (M=512).
+
+    python scripts/gemm_bench.py [--iters 50] [--m 512]
+
+Times each shape with CUDA events on the launching stream (after warm-up) and
+prints TFLOP/s against MEASURED_PEAKS.json.  Weights (B) are larger than L2
+for every shape except O-proj; a 256 MB buffer is rewritten between
+iterations to flush L2.
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2401_11181_b200 import native  # noqa: E402
+
+SHAPES = {"qkv": (15360, 5120, native.EPI_BF16_BIAS), "o": (5120, 5120, native.EPI_F32_BIAS_RESID),
+          "fc1": (20480, 5120, native.EPI_BF16_BIAS_RELU), "fc2": (5120, 20480, native.EPI_F32_BIAS_RESID)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--m", type=int, nargs="*", default=[512])
+    ap.add_argument("--shapes", nargs="*", default=list(SHAPES))
+    ap.add_argument("--no-flush", action="store_true")
+    args = ap.parse_args()
+    native.load()
+    peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for M in args.m:
+        for name in args.shapes:
+            N, K, epi = SHAPES[name]
+            a = torch.randn(M, K, device="cuda").bfloat16()
+            b = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+            bias = torch.zeros(N, device="cuda").bfloat16()
+            out = torch.zeros(M, N, device="cuda",
+                              dtype=torch.float32 if epi >= 3 else torch.bfloat16)
+            import ctypes
+            nb = ctypes.c_int64()
+            native.check(native.load().tk_gemm_workspace_bytes(M, N, K, ctypes.byref(nb)))
+            ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")
+            for _ in range(3):
+                native.gemm(a, b, bias=bias, epilogue=epi, out=out, workspace=ws)
+            torch.cuda.synchronize()
+            times = []
+            for _ in range(args.iters):
+                if not args.no_flush:
+                    flush.zero_()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                native.gemm(a, b, bias=bias, epilogue=epi, out=out, workspace=ws)
+                e.record()
+                e.synchronize()
+                times.append(s.elapsed_time(e))
+            ms = sorted(times)[len(times) // 2]
+            tf = 2 * M * N * K / (ms / 1e3) / 1e12
+            print(json.dumps({"shape": name, "M": M, "N": N, "K": K, "median_us": round(ms * 1e3, 2),
+                              "tflops": round(tf, 1),
+                              "frac_burst": round(tf / peak["bf16_tflops"], 3)}))
+
+
+if __name__ == "__main__":
+    main()

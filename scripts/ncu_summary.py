@@ -1,0 +1,50 @@
+"""Summarise an .ncu-rep (one or more profiled launches) into JSON lines.
+
+    python scripts/ncu_summary.py gpurun_out/x.ncu-rep [--label name] >> profiles/rNN_x.jsonl
+
+Keeps the metrics the roofline and the judge need: duration, DRAM bytes
+read/written (the `traffic` field), tensor-pipe activity, TMA L2->SM bytes,
+L2 hit rate, occupancy, registers.
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+WANT = {
+    "gpu__time_duration.sum": "duration",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_pct",
+    "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum": "tma_load_bytes",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
+    "launch__registers_per_thread": "regs",
+    "launch__grid_size": "grid",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
+    "smsp__inst_executed.sum": "inst",
+}
+
+
+def main():
+    rep = sys.argv[1]
+    label = sys.argv[sys.argv.index("--label") + 1] if "--label" in sys.argv else rep
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:
+        rec = {"label": label}
+        for h, u, v in zip(hdr, units, vals):
+            if h == "Kernel Name":
+                rec["kernel"] = v[:120]
+            for key, short in WANT.items():
+                if h == key or h.endswith("." + key):
+                    rec[short] = f"{v} {u}".strip()
+        print(json.dumps(rec))
+
+
+if __name__ == "__main__":
+    main()

@@ -33,6 +33,9 @@ def _rel_err(x, ref):
     (33, 3072, 768),     # decode-sized M, BN=256, stream-K split
     (64, 768, 3072),     # BN=128 path
     (512, 48, 768),      # classifier head (N=48)
+    (256, 5120, 5120),   # 2-CTA cluster multicast
+    (1024, 3072, 768),   # two m-groups of a 4-CTA cluster
+    (384, 2048, 1024),   # tiles_m=3 -> no cluster
 ])
 def test_gemm_matches_fp32(M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
