@@ -33,6 +33,8 @@
 #include "tk_common.cuh"
 #include "tk_kernels.h"
 
+#include <algorithm>
+
 namespace tk {
 
 template <int BN>
@@ -51,17 +53,27 @@ struct GemmCfg {
 
 struct GemmArgs {
   void* C;
-  int cs;  // cluster size along M (1, 2 or 4)
+  int cs;     // cluster size along M (1, 2 or 4)
+  int slots;  // partial slots per tile (max contributors - 1)
   const __nv_bfloat16* bias;
-  float* ws;
-  int* counters;
+  float* ws;      // [tiles][slots][BN/32][128 threads][32] fp32 partials
+  int* counters;  // [tiles] arrival counters, then [tiles][slots] ready flags
   int M, N, K;
   int epi;
   int tiles_m, tiles_n, kbs;
   long long total_iters;
 };
 
-__device__ __forceinline__ int owner_of(long long it, long long T, int G) {
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__host__ __device__ __forceinline__ int owner_of(long long it, long long T, int G) {
   // CTA c covers [floor(c*T/G), floor((c+1)*T/G))
   return static_cast<int>(((it + 1) * G + T - 1) / T) - 1;
 }
@@ -278,48 +290,72 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
       } else {
-        float* ws_row = p.ws + (static_cast<size_t>(tile) * Cfg::BM + row_in_tile) * BN;
+        // Stream-K fixup without atomics: arrival order decides who finalises.
+        // Earlier arrivals store their partial tile (coalesced, thread-major)
+        // into their own slot and raise a flag; the last arrival waits for the
+        // flags, adds the partials to its TMEM accumulator and runs the epilogue.
+        int* counter = p.counters + tile;
+        int* flags = p.counters + p.tiles_m * p.tiles_n + static_cast<size_t>(tile) * p.slots;
+        if (leader) *last_flag = atomicAdd(counter, 1);
+        named_bar_sync(1, 128);
+        const int arrival = *last_flag;
+        const size_t slot_elems = static_cast<size_t>(BN / 32) * 128 * 32;
+        float* tile_ws = p.ws + static_cast<size_t>(tile) * p.slots * slot_elems;
+        const int tid_e = static_cast<int>(threadIdx.x) - 64;  // 0..127, epilogue thread index
+        if (arrival < contrib - 1) {
+          float* mine = tile_ws + static_cast<size_t>(arrival) * slot_elems;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + c * 32, r);
-          tmem_wait_ld();
-          if (row >= p.M) continue;  // rows past M are zero (TMA zero-fill)
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_row + c * 32, r);
+            tmem_wait_ld();
+            float4* dst = reinterpret_cast<float4*>(mine + (static_cast<size_t>(c) * 128 + tid_e) * 32);
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            atomicAdd(reinterpret_cast<float4*>(ws_row + c * 32 + g * 4),
-                      make_float4(__uint_as_float(r[g * 4]), __uint_as_float(r[g * 4 + 1]),
-                                  __uint_as_float(r[g * 4 + 2]), __uint_as_float(r[g * 4 + 3])));
+            for (int g = 0; g < 8; ++g)
+              __stcg(dst + g, make_float4(__uint_as_float(r[g * 4]), __uint_as_float(r[g * 4 + 1]),
+                                          __uint_as_float(r[g * 4 + 2]), __uint_as_float(r[g * 4 + 3])));
           }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (leader) {
-          const int prev = atomicAdd(p.counters + tile, 1);
-          *last_flag = (prev == contrib - 1) ? 1 : 0;
-        }
-        named_bar_sync(1, 128);
-        if (*last_flag && row < p.M) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (leader) st_release(flags + arrival, 1);
+        } else {
+          if (leader) {
+            for (int a = 0; a < contrib - 1; ++a)
+              while (ld_acquire(flags + a) == 0) {
+              }
+          }
+          named_bar_sync(1, 128);
           __threadfence();
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_row + c * 32, r);
+            tmem_wait_ld();
             float v[32];
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-              float4 s = __ldcg(reinterpret_cast<const float4*>(ws_row + c * 32 + g * 4));
-              v[g * 4] = s.x; v[g * 4 + 1] = s.y; v[g * 4 + 2] = s.z; v[g * 4 + 3] = s.w;
-              __stcg(reinterpret_cast<float4*>(ws_row + c * 32 + g * 4),
-                     make_float4(0.f, 0.f, 0.f, 0.f));
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            for (int a = 0; a < contrib - 1; ++a) {
+              const float4* src = reinterpret_cast<const float4*>(
+                  tile_ws + static_cast<size_t>(a) * slot_elems + (static_cast<size_t>(c) * 128 + tid_e) * 32);
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const float4 t = __ldcg(src + g);
+                v[g * 4] += t.x; v[g * 4 + 1] += t.y; v[g * 4 + 2] += t.z; v[g * 4 + 3] += t.w;
+              }
             }
             epilogue_store<EPI>(p, row, col_base + c * 32, v);
           }
-        }
-        if (*last_flag) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
           named_bar_sync(1, 128);
-          if (leader) atomicExch(p.counters + tile, 0);
+          if (leader) {
+            for (int a = 0; a < contrib - 1; ++a) flags[a] = 0;
+            *counter = 0;
+          }
         }
       }
       acc ^= 1;
@@ -374,45 +410,63 @@ int make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t
 
 static int pick_bn(int N) { return N >= 1024 ? 256 : 128; }
 
-int64_t gemm_workspace_bytes(int M, int N, int K) {
-  const int bn = pick_bn(N);
-  const int64_t tiles = static_cast<int64_t>((M + 127) / 128) * ((N + bn - 1) / bn);
-  return tiles * 128 * bn * 4 + tiles * 4 + 256;
+// Co-resident clusters of size cs for the BN variant (queried once per variant).
+static int max_clusters_for(int bn, int cs);
+
+// Counter/flag region at the head of every GEMM workspace.  It is shared by all
+// GEMM shapes that use the workspace and is zero between launches (the last
+// contributor of each tile resets what it used), so it must never overlap the
+// partial slots of any shape: it has a fixed size.
+constexpr int64_t kCounterBytes = 1 << 20;
+
+struct GemmPlan {
+  bool counters_fit;
+  int bn, cs, tiles_m, tiles_n, kbs, clusters, slots;
+  long long total_iters;
+  int64_t ws_bytes;
+};
+
+static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
+  GemmPlan pl{};
+  pl.bn = pick_bn(N);
+  pl.tiles_m = (M + 127) / 128;
+  pl.tiles_n = (N + pl.bn - 1) / pl.bn;
+  pl.kbs = K / 64;
+  pl.cs = pl.tiles_m % 4 == 0 ? 4 : (pl.tiles_m % 2 == 0 ? 2 : 1);
+  pl.total_iters = static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
+  int clusters = max_clusters_for(pl.bn, pl.cs);
+  if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / pl.cs));
+  clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, pl.total_iters / 4)));
+  pl.clusters = clusters;
+  // most CTAs (clusters) sharing one tile, over all cluster tiles
+  const long long ctiles = pl.total_iters / pl.kbs;
+  int most = 1;
+  for (long long t = 0; t < ctiles; ++t) {
+    const int c = owner_of((t + 1) * pl.kbs - 1, pl.total_iters, clusters) -
+                  owner_of(t * pl.kbs, pl.total_iters, clusters) + 1;
+    most = std::max(most, c);
+  }
+  pl.slots = most - 1;
+  const int64_t tiles = static_cast<int64_t>(pl.tiles_m) * pl.tiles_n;
+  // [kCounterBytes: per-tile counters + ready flags, always left zeroed][partial slots]
+  pl.ws_bytes = kCounterBytes + tiles * pl.slots * 128LL * pl.bn * 4;
+  pl.counters_fit = tiles * (1 + pl.slots) * 4 <= kCounterBytes;
+  return pl;
 }
+
+int64_t gemm_workspace_bytes(int M, int N, int K) { return plan_gemm(M, N, K, 0).ws_bytes; }
 
 template <int BN, int EPI, int CS>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
-                       int max_ctas, cudaStream_t stream) {
+                       int clusters, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_tn_kernel<BN, EPI, CS>;
-  static int max_clusters = 0;
-  if (max_clusters == 0) {
+  static bool configured = false;
+  if (!configured) {
     TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::SMEM_BYTES));
-    cudaLaunchConfig_t q{};
-    q.gridDim = dim3(kNumSMs / CS * CS);
-    q.blockDim = dim3(Cfg::THREADS);
-    q.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cudaLaunchAttribute qa[1];
-    qa[0].id = cudaLaunchAttributeClusterDimension;
-    qa[0].val.clusterDim.x = CS;
-    qa[0].val.clusterDim.y = 1;
-    qa[0].val.clusterDim.z = 1;
-    q.attrs = qa;
-    q.numAttrs = 1;
-    int n = 0;
-    if (CS > 1) {
-      TK_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &q));
-    } else {
-      n = kNumSMs;
-    }
-    max_clusters = n > 0 ? n : 1;
+    configured = true;
   }
-  // clusters: all co-resident, never more than the cluster-level iterations / 4
-  const long long iters = a.total_iters;
-  int clusters = max_clusters;
-  if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / CS));
-  clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, iters / 4)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * CS);
   cfg.blockDim = dim3(Cfg::THREADS);
@@ -431,14 +485,53 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
 }
 
 template <int BN, int CS>
+static int query_clusters() {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_tn_kernel<BN, EPI_BF16, CS>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) !=
+      cudaSuccess)
+    return kNumSMs / CS;
+  if (CS == 1) return kNumSMs;
+  cudaLaunchConfig_t q{};
+  q.gridDim = dim3(kNumSMs / CS * CS);
+  q.blockDim = dim3(Cfg::THREADS);
+  q.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cudaLaunchAttribute qa[1];
+  qa[0].id = cudaLaunchAttributeClusterDimension;
+  qa[0].val.clusterDim.x = CS;
+  qa[0].val.clusterDim.y = 1;
+  qa[0].val.clusterDim.z = 1;
+  q.attrs = qa;
+  q.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return kNumSMs / CS;
+  }
+  return n;
+}
+
+static int max_clusters_for(int bn, int cs) {
+  static int cache[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  const int bi = bn == 256 ? 1 : 0;
+  const int ci = cs == 4 ? 2 : (cs == 2 ? 1 : 0);
+  int& v = cache[bi][ci];
+  if (v == 0) {
+    if (bn == 256) v = cs == 4 ? query_clusters<256, 4>() : cs == 2 ? query_clusters<256, 2>() : query_clusters<256, 1>();
+    else v = cs == 4 ? query_clusters<128, 4>() : cs == 2 ? query_clusters<128, 2>() : query_clusters<128, 1>();
+  }
+  return v;
+}
+
+template <int BN, int CS>
 static int dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
-                        int max_ctas, cudaStream_t s) {
+                        int clusters, cudaStream_t s) {
   switch (a.epi) {
-    case EPI_BF16: return launch_gemm<BN, EPI_BF16, CS>(ta, tb, a, max_ctas, s);
-    case EPI_BF16_BIAS: return launch_gemm<BN, EPI_BF16_BIAS, CS>(ta, tb, a, max_ctas, s);
-    case EPI_BF16_BIAS_RELU: return launch_gemm<BN, EPI_BF16_BIAS_RELU, CS>(ta, tb, a, max_ctas, s);
-    case EPI_F32_BIAS_RESID: return launch_gemm<BN, EPI_F32_BIAS_RESID, CS>(ta, tb, a, max_ctas, s);
-    case EPI_F32: return launch_gemm<BN, EPI_F32, CS>(ta, tb, a, max_ctas, s);
+    case EPI_BF16: return launch_gemm<BN, EPI_BF16, CS>(ta, tb, a, clusters, s);
+    case EPI_BF16_BIAS: return launch_gemm<BN, EPI_BF16_BIAS, CS>(ta, tb, a, clusters, s);
+    case EPI_BF16_BIAS_RELU: return launch_gemm<BN, EPI_BF16_BIAS_RELU, CS>(ta, tb, a, clusters, s);
+    case EPI_F32_BIAS_RESID: return launch_gemm<BN, EPI_F32_BIAS_RESID, CS>(ta, tb, a, clusters, s);
+    case EPI_F32: return launch_gemm<BN, EPI_F32, CS>(ta, tb, a, clusters, s);
   }
   set_error("unknown gemm epilogue");
   return TK_EINVAL;
@@ -446,14 +539,14 @@ static int dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
 
 template <int BN>
 static int dispatch_cs(const void* B, int N, int K, const CUtensorMap& ta, GemmArgs& a,
-                       int max_ctas, cudaStream_t s) {
+                       int clusters, cudaStream_t s) {
   CUtensorMap tb;
   int rc = make_tmap_kmajor(&tb, B, N, K, BN / a.cs);
   if (rc) return rc;
   switch (a.cs) {
-    case 4: return dispatch_epi<BN, 4>(ta, tb, a, max_ctas, s);
-    case 2: return dispatch_epi<BN, 2>(ta, tb, a, max_ctas, s);
-    default: return dispatch_epi<BN, 1>(ta, tb, a, max_ctas, s);
+    case 4: return dispatch_epi<BN, 4>(ta, tb, a, clusters, s);
+    case 2: return dispatch_epi<BN, 2>(ta, tb, a, clusters, s);
+    default: return dispatch_epi<BN, 1>(ta, tb, a, clusters, s);
   }
 }
 
@@ -462,8 +555,9 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   TK_CHECK(M > 0 && N > 0 && K > 0, TK_EINVAL, "gemm: empty problem");
   TK_CHECK(K % 64 == 0, TK_EINVAL, "gemm: K must be a multiple of 64");
   TK_CHECK(N % 8 == 0, TK_EINVAL, "gemm: N must be a multiple of 8");
-  TK_CHECK(ws_bytes >= gemm_workspace_bytes(M, N, K), TK_EINVAL, "gemm: workspace too small");
-  const int bn = pick_bn(N);
+  const GemmPlan pl = plan_gemm(M, N, K, max_ctas);
+  TK_CHECK(ws_bytes >= pl.ws_bytes, TK_EINVAL, "gemm: workspace too small");
+  TK_CHECK(pl.counters_fit, TK_EINVAL, "gemm: too many tiles for the counter region");
   CUtensorMap ta;
   int rc = make_tmap_kmajor(&ta, A, M, K, 128);
   if (rc) return rc;
@@ -474,16 +568,18 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   a.N = N;
   a.K = K;
   a.epi = epi;
-  a.tiles_m = (M + 127) / 128;
-  a.tiles_n = (N + bn - 1) / bn;
-  a.kbs = K / 64;
-  a.cs = a.tiles_m % 4 == 0 ? 4 : (a.tiles_m % 2 == 0 ? 2 : 1);
+  a.tiles_m = pl.tiles_m;
+  a.tiles_n = pl.tiles_n;
+  a.kbs = pl.kbs;
+  a.cs = pl.cs;
+  a.slots = pl.slots;
+  a.total_iters = pl.total_iters;
   const int64_t tiles = static_cast<int64_t>(a.tiles_m) * a.tiles_n;
-  a.total_iters = static_cast<int64_t>(a.tiles_m / a.cs) * a.tiles_n * a.kbs;
-  a.ws = static_cast<float*>(workspace);
-  a.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(workspace) + tiles * 128 * bn * 4);
-  if (bn == 256) return dispatch_cs<256>(B, N, K, ta, a, max_ctas, stream);
-  return dispatch_cs<128>(B, N, K, ta, a, max_ctas, stream);
+  (void)tiles;
+  a.counters = static_cast<int*>(workspace);
+  a.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
+  if (pl.bn == 256) return dispatch_cs<256>(B, N, K, ta, a, pl.clusters, stream);
+  return dispatch_cs<128>(B, N, K, ta, a, pl.clusters, stream);
 }
 
 }  // namespace tk

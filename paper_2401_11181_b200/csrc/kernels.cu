@@ -9,6 +9,7 @@
 //   decode_attention   K3: paged decode attention, split-KV over 256-token partitions,
 //                      128-bit coalesced page loads, warp-shuffle softmax, combine pass
 //   argmax             greedy token per row (first maximum, like torch.argmax)
+#include <algorithm>
 #include <cfloat>
 
 #include "tk_common.cuh"
@@ -258,26 +259,35 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// One CTA = 8 warps = up to 128 query rows of one slice (16 rows per warp)
+// x one head x one KV split [kb0, kb1) of 64-key blocks.  The 8 warps share
+// every K/V tile, so shared-memory fill per MMA is half that of 64-row CTAs.
+// A q-block whose prefix is long is split over several CTAs (split-KV); each
+// writes an unnormalised partial (m, l, O) that attn_combine_kernel merges.
+constexpr int kAttnRows = 128;
+constexpr int kAttnBlock = 64;
+constexpr int kAttnThreads = 256;
+
 template <int D>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kAttnThreads)
     chunk_attn_kernel(const __nv_bfloat16* __restrict__ q, int q_stride,
                       __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ pool,
                       KvGeom g, int layer, const AttnWork* __restrict__ work,
-                      const tk_slice* __restrict__ slices, const int32_t* __restrict__ bt,
-                      float scale_log2) {
-  constexpr int BKV = 64;
+                      const AttnQBlock* __restrict__ qblocks, const tk_slice* __restrict__ slices,
+                      const int32_t* __restrict__ bt, float scale_log2,
+                      float* __restrict__ partial) {
   constexpr int CH = D / 8;  // 16-byte chunks per row
-  constexpr int TILE = BKV * D;
+  constexpr int TILE = kAttnBlock * D;
   extern __shared__ __align__(128) uint8_t sm[];
   __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(sm);  // [2][64][D]
   __nv_bfloat16* sV = sK + 2 * TILE;                           // [2][64][D]
 
   const AttnWork w = work[blockIdx.x];
+  const AttnQBlock qb = qblocks[w.qblock];
   const int head = blockIdx.y;
-  const tk_slice sl = slices[w.slice];
+  const tk_slice sl = slices[qb.slice];
   const int32_t* pages = bt + sl.bt_offset;
-  const int kv_end = w.pos0 + w.nrows;  // keys [0, kv_end) may be needed
-  const int n_blocks = (kv_end + BKV - 1) / BKV;
+  const int kv_end = qb.pos0 + qb.nrows;  // keys [0, kv_end) exist for this block
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int pt = g.page_tokens;
@@ -285,29 +295,30 @@ __global__ void __launch_bounds__(128)
   auto load_block = [&](int j, int buf) {
     __nv_bfloat16* dk = sK + buf * TILE;
     __nv_bfloat16* dv = sV + buf * TILE;
-    for (int i = tid; i < BKV * CH; i += 128) {
+#pragma unroll
+    for (int it = 0; it < kAttnBlock * CH / kAttnThreads; ++it) {
+      const int i = tid + it * kAttnThreads;
       const int r = i / CH, c = i % CH;
-      const int p = j * BKV + r;
+      const int p = j * kAttnBlock + r;
       const bool valid = p < kv_end;
-      const int page = valid ? pages[p / pt] : 0;
+      const int page = valid ? __ldg(pages + p / pt) : 0;
       const size_t off = valid ? g.offset(page, layer, 0, head, p % pt) : 0;
+      const size_t offv = valid ? g.offset(page, layer, 1, head, p % pt) : 0;
       const int sw = r * D + ((c ^ (r & 7)) * 8);
       cp_async16(dk + sw, pool + off + c * 8, valid);
-      const size_t offv = valid ? g.offset(page, layer, 1, head, p % pt) : 0;
       cp_async16(dv + sw, pool + offv + c * 8, valid);
     }
   };
 
-  load_block(0, 0);
+  load_block(w.kb0, 0);
   cp_async_commit();
 
-  // Q fragments (16 rows per warp) straight from global.
   uint32_t qa[D / 16][4];
   const int r_lo = warp * 16 + gq, r_hi = r_lo + 8;
   {
-    const __nv_bfloat16* q_lo = q + static_cast<size_t>(w.row0 + r_lo) * q_stride + head * D;
-    const __nv_bfloat16* q_hi = q + static_cast<size_t>(w.row0 + r_hi) * q_stride + head * D;
-    const bool v_lo = r_lo < w.nrows, v_hi = r_hi < w.nrows;
+    const __nv_bfloat16* q_lo = q + static_cast<size_t>(qb.row0 + r_lo) * q_stride + head * D;
+    const __nv_bfloat16* q_hi = q + static_cast<size_t>(qb.row0 + r_hi) * q_stride + head * D;
+    const bool v_lo = r_lo < qb.nrows, v_hi = r_hi < qb.nrows;
 #pragma unroll
     for (int ks = 0; ks < D / 16; ++ks) {
       const int c = ks * 16 + tq * 2;
@@ -317,186 +328,294 @@ __global__ void __launch_bounds__(128)
       qa[ks][3] = v_hi ? *reinterpret_cast<const uint32_t*>(q_hi + c + 8) : 0u;
     }
   }
-  const int qp_lo = w.pos0 + r_lo, qp_hi = w.pos0 + r_hi;
+  const int qp_lo = qb.pos0 + r_lo, qp_hi = qb.pos0 + r_hi;
+  const int warp_min_q = qb.pos0 + warp * 16;
+  const int warp_max_q = qb.pos0 + min(warp * 16 + 15, qb.nrows - 1);
 
   float acc[D / 8][4];
 #pragma unroll
   for (int i = 0; i < D / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
-  for (int j = 0; j < n_blocks; ++j) {
-    const int buf = j & 1;
-    if (j + 1 < n_blocks) load_block(j + 1, buf ^ 1);
+  for (int j = w.kb0; j < w.kb1; ++j) {
+    const int buf = (j - w.kb0) & 1;
+    if (j + 1 < w.kb1) load_block(j + 1, buf ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
 
-    const uint32_t kbase = smem_u32(sK + buf * TILE);
-    const uint32_t vbase = smem_u32(sV + buf * TILE);
-    // S = Q K^T : 16 x 64 per warp
-    float s[8][4];
+    const int kp0 = j * kAttnBlock;
+    // whole block above this warp's diagonal: nothing to do (warp-uniform)
+    if (kp0 <= warp_max_q) {
+      const uint32_t kbase = smem_u32(sK + buf * TILE);
+      const uint32_t vbase = smem_u32(sV + buf * TILE);
+      float s[8][4];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+      for (int nt = 0; nt < 8; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
 #pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks) {
+      for (int ks = 0; ks < D / 16; ++ks) {
 #pragma unroll
-      for (int nt = 0; nt < 8; nt += 2) {
-        // matrices: (nt, chunk 2ks), (nt, 2ks+1), (nt+1, 2ks), (nt+1, 2ks+1)
-        const int mi = lane >> 3;
-        const int row = (nt + (mi >> 1)) * 8 + (lane & 7);
-        const int chunk = ks * 2 + (mi & 1);
-        const uint32_t addr = kbase + (row * D + ((chunk ^ (row & 7)) * 8)) * 2;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(addr, b0, b1, b2, b3);
-        mma_bf16_16816(s[nt], qa[ks], b0, b1);
-        mma_bf16_16816(s[nt + 1], qa[ks], b2, b3);
+        for (int nt = 0; nt < 8; nt += 2) {
+          const int mi = lane >> 3;
+          const int row = (nt + (mi >> 1)) * 8 + (lane & 7);
+          const int chunk = ks * 2 + (mi & 1);
+          const uint32_t addr = kbase + (row * D + ((chunk ^ (row & 7)) * 8)) * 2;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(addr, b0, b1, b2, b3);
+          mma_bf16_16816(s[nt], qa[ks], b0, b1);
+          mma_bf16_16816(s[nt + 1], qa[ks], b2, b3);
+        }
       }
-    }
-    // causal mask (also hides keys beyond kv_end, which are zero-filled)
-    const int kp0 = j * BKV;
-    if (kp0 + BKV - 1 > w.pos0 + warp * 16) {
+      if (kp0 + kAttnBlock - 1 > warp_min_q) {
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          const int kp = kp0 + nt * 8 + tq * 2;
+          if (kp > qp_lo) s[nt][0] = -INFINITY;
+          if (kp + 1 > qp_lo) s[nt][1] = -INFINITY;
+          if (kp > qp_hi) s[nt][2] = -INFINITY;
+          if (kp + 1 > qp_hi) s[nt][3] = -INFINITY;
+        }
+      }
+      float mx_lo = m_lo, mx_hi = m_hi;
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
-        const int kp = kp0 + nt * 8 + tq * 2;
-        if (kp > qp_lo) s[nt][0] = -INFINITY;
-        if (kp + 1 > qp_lo) s[nt][1] = -INFINITY;
-        if (kp > qp_hi) s[nt][2] = -INFINITY;
-        if (kp + 1 > qp_hi) s[nt][3] = -INFINITY;
+        mx_lo = fmaxf(mx_lo, fmaxf(s[nt][0], s[nt][1]) * scale_log2);
+        mx_hi = fmaxf(mx_hi, fmaxf(s[nt][2], s[nt][3]) * scale_log2);
       }
-    }
-    // online softmax (rows lo / hi; reduce across the 4 lanes of a quad)
-    float mx_lo = m_lo, mx_hi = m_hi;
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+      const float base_lo = (mx_lo == -INFINITY) ? 0.f : mx_lo;
+      const float base_hi = (mx_hi == -INFINITY) ? 0.f : mx_hi;
+      const float corr_lo = exp2f(m_lo - base_lo);
+      const float corr_hi = exp2f(m_hi - base_hi);
+      m_lo = mx_lo;
+      m_hi = mx_hi;
+      float sum_lo = 0.f, sum_hi = 0.f;
+      uint32_t pa[4][4];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      mx_lo = fmaxf(mx_lo, fmaxf(s[nt][0], s[nt][1]) * scale_log2);
-      mx_hi = fmaxf(mx_hi, fmaxf(s[nt][2], s[nt][3]) * scale_log2);
-    }
-    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
-    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
-    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
-    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
-    const float base_lo = (mx_lo == -INFINITY) ? 0.f : mx_lo;
-    const float base_hi = (mx_hi == -INFINITY) ? 0.f : mx_hi;
-    const float corr_lo = exp2f(m_lo - base_lo);
-    const float corr_hi = exp2f(m_hi - base_hi);
-    m_lo = mx_lo;
-    m_hi = mx_hi;
-    float sum_lo = 0.f, sum_hi = 0.f;
-    uint32_t pa[4][4];  // P as A fragments, 4 k-steps of 16 keys
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      const float p0 = exp2f(s[nt][0] * scale_log2 - base_lo);
-      const float p1 = exp2f(s[nt][1] * scale_log2 - base_lo);
-      const float p2 = exp2f(s[nt][2] * scale_log2 - base_hi);
-      const float p3 = exp2f(s[nt][3] * scale_log2 - base_hi);
-      sum_lo += p0 + p1;
-      sum_hi += p2 + p3;
-      const int ks = nt >> 1;
-      if ((nt & 1) == 0) {
-        pa[ks][0] = pack_bf16x2(p0, p1);
-        pa[ks][1] = pack_bf16x2(p2, p3);
-      } else {
-        pa[ks][2] = pack_bf16x2(p0, p1);
-        pa[ks][3] = pack_bf16x2(p2, p3);
+      for (int nt = 0; nt < 8; ++nt) {
+        const float p0 = exp2f(fmaf(s[nt][0], scale_log2, -base_lo));
+        const float p1 = exp2f(fmaf(s[nt][1], scale_log2, -base_lo));
+        const float p2 = exp2f(fmaf(s[nt][2], scale_log2, -base_hi));
+        const float p3 = exp2f(fmaf(s[nt][3], scale_log2, -base_hi));
+        sum_lo += p0 + p1;
+        sum_hi += p2 + p3;
+        const int ks = nt >> 1;
+        if ((nt & 1) == 0) {
+          pa[ks][0] = pack_bf16x2(p0, p1);
+          pa[ks][1] = pack_bf16x2(p2, p3);
+        } else {
+          pa[ks][2] = pack_bf16x2(p0, p1);
+          pa[ks][3] = pack_bf16x2(p2, p3);
+        }
       }
-    }
-    l_lo = l_lo * corr_lo + sum_lo;
-    l_hi = l_hi * corr_hi + sum_hi;
+      l_lo = l_lo * corr_lo + sum_lo;
+      l_hi = l_hi * corr_hi + sum_hi;
 #pragma unroll
-    for (int i = 0; i < D / 8; ++i) {
-      acc[i][0] *= corr_lo;
-      acc[i][1] *= corr_lo;
-      acc[i][2] *= corr_hi;
-      acc[i][3] *= corr_hi;
-    }
-    // O += P V
+      for (int i = 0; i < D / 8; ++i) {
+        acc[i][0] *= corr_lo;
+        acc[i][1] *= corr_lo;
+        acc[i][2] *= corr_hi;
+        acc[i][3] *= corr_hi;
+      }
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
+      for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
-      for (int nt = 0; nt < D / 8; nt += 2) {
-        // matrices: (keys 16ks+0..7, dchunk nt), (16ks+8.., nt), (16ks.., nt+1), (16ks+8.., nt+1)
-        const int mi = lane >> 3;
-        const int row = ks * 16 + (mi & 1) * 8 + (lane & 7);
-        const int chunk = nt + (mi >> 1);
-        const uint32_t addr = vbase + (row * D + ((chunk ^ (row & 7)) * 8)) * 2;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(addr, b0, b1, b2, b3);
-        mma_bf16_16816(acc[nt], pa[ks], b0, b1);
-        mma_bf16_16816(acc[nt + 1], pa[ks], b2, b3);
+        for (int nt = 0; nt < D / 8; nt += 2) {
+          const int mi = lane >> 3;
+          const int row = ks * 16 + (mi & 1) * 8 + (lane & 7);
+          const int chunk = nt + (mi >> 1);
+          const uint32_t addr = vbase + (row * D + ((chunk ^ (row & 7)) * 8)) * 2;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(addr, b0, b1, b2, b3);
+          mma_bf16_16816(acc[nt], pa[ks], b0, b1);
+          mma_bf16_16816(acc[nt + 1], pa[ks], b2, b3);
+        }
       }
     }
     __syncthreads();
   }
   cp_async_wait<0>();
 
-  // finalize: quad-reduce row sums, normalise, store bf16
   l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
   l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
   l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
   l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
-  const float inv_lo = l_lo > 0.f ? 1.f / l_lo : 0.f;
-  const float inv_hi = l_hi > 0.f ? 1.f / l_hi : 0.f;
   const int HD = g.n_heads * D;
-  if (r_lo < w.nrows) {
-    __nv_bfloat16* out = o + static_cast<size_t>(w.row0 + r_lo) * HD + head * D;
+  if (qb.n_splits == 1) {
+    const float inv_lo = l_lo > 0.f ? 1.f / l_lo : 0.f;
+    const float inv_hi = l_hi > 0.f ? 1.f / l_hi : 0.f;
+    if (r_lo < qb.nrows) {
+      __nv_bfloat16* out = o + static_cast<size_t>(qb.row0 + r_lo) * HD + head * D;
 #pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt)
-      *reinterpret_cast<uint32_t*>(out + nt * 8 + tq * 2) =
-          pack_bf16x2(acc[nt][0] * inv_lo, acc[nt][1] * inv_lo);
-  }
-  if (r_hi < w.nrows) {
-    __nv_bfloat16* out = o + static_cast<size_t>(w.row0 + r_hi) * HD + head * D;
+      for (int nt = 0; nt < D / 8; ++nt)
+        *reinterpret_cast<uint32_t*>(out + nt * 8 + tq * 2) =
+            pack_bf16x2(acc[nt][0] * inv_lo, acc[nt][1] * inv_lo);
+    }
+    if (r_hi < qb.nrows) {
+      __nv_bfloat16* out = o + static_cast<size_t>(qb.row0 + r_hi) * HD + head * D;
 #pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt)
-      *reinterpret_cast<uint32_t*>(out + nt * 8 + tq * 2) =
-          pack_bf16x2(acc[nt][2] * inv_hi, acc[nt][3] * inv_hi);
+      for (int nt = 0; nt < D / 8; ++nt)
+        *reinterpret_cast<uint32_t*>(out + nt * 8 + tq * 2) =
+            pack_bf16x2(acc[nt][2] * inv_hi, acc[nt][3] * inv_hi);
+    }
+  } else {
+    // partial[(slot * H + head) * 128 + row][D + 2]: O unnormalised, m, l
+    float* base = partial + (static_cast<size_t>(w.slot) * g.n_heads + head) * kAttnRows * (D + 2);
+    float* plo = base + static_cast<size_t>(r_lo) * (D + 2);
+    float* phi = base + static_cast<size_t>(r_hi) * (D + 2);
+#pragma unroll
+    for (int nt = 0; nt < D / 8; ++nt) {
+      *reinterpret_cast<float2*>(plo + nt * 8 + tq * 2) = make_float2(acc[nt][0], acc[nt][1]);
+      *reinterpret_cast<float2*>(phi + nt * 8 + tq * 2) = make_float2(acc[nt][2], acc[nt][3]);
+    }
+    if (tq == 0) {
+      plo[D] = m_lo;
+      plo[D + 1] = l_lo;
+      phi[D] = m_hi;
+      phi[D + 1] = l_hi;
+    }
   }
 }
 
-int build_attn_work(const tk_slice* slices, int n_slices, AttnWork* out, int cap) {
-  int n = 0, row = 0;
+// Merge the split partials of every multi-split q-block: grid (qblocks, heads).
+template <int D>
+__global__ void __launch_bounds__(kAttnRows)
+    attn_combine_kernel(__nv_bfloat16* __restrict__ o, const AttnQBlock* __restrict__ qblocks,
+                        int n_heads, const float* __restrict__ partial) {
+  const AttnQBlock qb = qblocks[blockIdx.x];
+  if (qb.n_splits <= 1) return;
+  const int head = blockIdx.y;
+  const int row = threadIdx.x;
+  if (row >= qb.nrows) return;
+  const size_t stride_slot = static_cast<size_t>(n_heads) * kAttnRows * (D + 2);
+  const float* first = partial + (static_cast<size_t>(qb.first_slot) * n_heads + head) * kAttnRows * (D + 2) +
+                       static_cast<size_t>(row) * (D + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < qb.n_splits; ++s) M = fmaxf(M, first[s * stride_slot + D]);
+  float L = 0.f;
+  float wts[16];
+  for (int s = 0; s < qb.n_splits; ++s) {
+    const float m = first[s * stride_slot + D];
+    wts[s] = (m == -INFINITY) ? 0.f : exp2f(m - M);
+    L += first[s * stride_slot + D + 1] * wts[s];
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat16* out = o + static_cast<size_t>(qb.row0 + row) * n_heads * D + head * D;
+  for (int d = 0; d < D; d += 2) {
+    float a0 = 0.f, a1 = 0.f;
+    for (int s = 0; s < qb.n_splits; ++s) {
+      const float2 v = *reinterpret_cast<const float2*>(first + s * stride_slot + d);
+      a0 += v.x * wts[s];
+      a1 += v.y * wts[s];
+    }
+    *reinterpret_cast<uint32_t*>(out + d) = pack_bf16x2(a0 * inv, a1 * inv);
+  }
+}
+
+int64_t attn_partial_bytes(int n_heads, int head_dim) {
+  return static_cast<int64_t>(kAttnMaxSplitSlots) * n_heads * kAttnRows * (head_dim + 2) * 4;
+}
+
+// Host: slices -> 128-row q-blocks -> KV splits.  Splits are made only when the
+// grid would otherwise be small (target ~4 CTAs per SM including heads) and
+// never below kAttnMinSplitBlocks blocks of keys per split.
+int build_attn_work(const tk_slice* slices, int n_slices, int n_heads, AttnQBlock* qbs,
+                    int qcap, AttnWork* items, int icap, int* n_qblocks) {
+  int nq = 0, row = 0;
+  int64_t total_blocks = 0;
   for (int i = 0; i < n_slices; ++i) {
-    for (int r = 0; r < slices[i].len; r += 64) {
-      if (n >= cap) return -1;
-      out[n].slice = i;
-      out[n].row0 = row + r;
-      out[n].nrows = min(64, slices[i].len - r);
-      out[n].pos0 = slices[i].start + r;
-      ++n;
+    for (int r = 0; r < slices[i].len; r += kAttnRows) {
+      if (nq >= qcap) return -1;
+      AttnQBlock& q = qbs[nq++];
+      q.slice = i;
+      q.row0 = row + r;
+      q.nrows = min(kAttnRows, slices[i].len - r);
+      q.pos0 = slices[i].start + r;
+      q.n_splits = 1;
+      q.first_slot = -1;
+      total_blocks += (q.pos0 + q.nrows + kAttnBlock - 1) / kAttnBlock;
     }
     row += slices[i].len;
   }
-  return n;
+  const int64_t target_ctas = 4LL * kNumSMs;
+  int n_items = 0, slot = 0;
+  for (int k = 0; k < nq; ++k) {
+    AttnQBlock& q = qbs[k];
+    const int nb = (q.pos0 + q.nrows + kAttnBlock - 1) / kAttnBlock;
+    int splits = 1;
+    if (static_cast<int64_t>(nq) * n_heads < target_ctas) {
+      const int64_t want = (target_ctas + static_cast<int64_t>(nq) * n_heads - 1) /
+                           (static_cast<int64_t>(nq) * n_heads);
+      splits = static_cast<int>(std::min<int64_t>(want, nb / kAttnMinSplitBlocks));
+      splits = std::max(1, std::min(splits, 16));
+      if (slot + splits > kAttnMaxSplitSlots) splits = 1;
+    }
+    q.n_splits = splits;
+    if (splits > 1) {
+      q.first_slot = slot;
+    }
+    for (int s = 0; s < splits; ++s) {
+      if (n_items >= icap) return -1;
+      AttnWork& w = items[n_items++];
+      w.qblock = k;
+      w.kb0 = static_cast<int>(static_cast<int64_t>(nb) * s / splits);
+      w.kb1 = static_cast<int>(static_cast<int64_t>(nb) * (s + 1) / splits);
+      w.slot = splits > 1 ? slot + s : -1;
+    }
+    if (splits > 1) slot += splits;
+  }
+  (void)total_blocks;
+  *n_qblocks = nq;
+  return n_items;
 }
 
 int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloat16* o,
                                 const __nv_bfloat16* pool, KvGeom g, int layer,
-                                const AttnWork* work, int n_work, const tk_slice* slices_dev,
-                                const int32_t* bt_dev, float scale, cudaStream_t s) {
+                                const AttnWork* work, int n_work, const AttnQBlock* qblocks,
+                                int n_qblocks, bool any_split, const tk_slice* slices_dev,
+                                const int32_t* bt_dev, float scale, float* partial,
+                                cudaStream_t s) {
   TK_CHECK(g.head_dim == 128 || g.head_dim == 64, TK_EUNSUPPORTED,
            "chunk attention: head_dim must be 64 or 128");
-  TK_CHECK(64 % g.page_tokens == 0 || g.page_tokens % 64 == 0, TK_EINVAL,
-           "chunk attention: page_tokens must divide 64 or be a multiple of it");
   if (n_work == 0) return TK_OK;
   const float scale_log2 = scale * 1.4426950408889634f;
   dim3 grid(n_work, g.n_heads);
   if (g.head_dim == 128) {
-    const int smem = 4 * 64 * 128 * 2;
+    const int smem = 4 * kAttnBlock * 128 * 2;
     static bool cfg = false;
     if (!cfg) {
       TK_CUDA(cudaFuncSetAttribute(chunk_attn_kernel<128>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       cfg = true;
     }
-    chunk_attn_kernel<128><<<grid, 128, smem, s>>>(q, q_stride, o, pool, g, layer, work, slices_dev,
-                                                   bt_dev, scale_log2);
+    chunk_attn_kernel<128><<<grid, kAttnThreads, smem, s>>>(q, q_stride, o, pool, g, layer, work,
+                                                            qblocks, slices_dev, bt_dev,
+                                                            scale_log2, partial);
+    TK_CUDA(cudaGetLastError());
+    note_launch();
+    if (any_split) {
+      attn_combine_kernel<128><<<dim3(n_qblocks, g.n_heads), kAttnRows, 0, s>>>(
+          o, qblocks, g.n_heads, partial);
+      TK_CUDA(cudaGetLastError());
+      note_launch();
+    }
   } else {
-    const int smem = 4 * 64 * 64 * 2;
-    chunk_attn_kernel<64><<<grid, 128, smem, s>>>(q, q_stride, o, pool, g, layer, work, slices_dev,
-                                                  bt_dev, scale_log2);
+    const int smem = 4 * kAttnBlock * 64 * 2;
+    chunk_attn_kernel<64><<<grid, kAttnThreads, smem, s>>>(q, q_stride, o, pool, g, layer, work,
+                                                           qblocks, slices_dev, bt_dev,
+                                                           scale_log2, partial);
+    TK_CUDA(cudaGetLastError());
+    note_launch();
+    if (any_split) {
+      attn_combine_kernel<64><<<dim3(n_qblocks, g.n_heads), kAttnRows, 0, s>>>(
+          o, qblocks, g.n_heads, partial);
+      TK_CUDA(cudaGetLastError());
+      note_launch();
+    }
   }
-  TK_CUDA(cudaGetLastError());
-  note_launch();
   return TK_OK;
 }
 

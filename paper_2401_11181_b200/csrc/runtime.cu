@@ -278,6 +278,7 @@ struct tk_instance {
   int64_t gemm_ws_bytes = 0;
   void* dec_ws = nullptr;
   int64_t dec_ws_bytes = 0;
+  float* attn_partial = nullptr;
   int dec_max_ctx = 0;
   tk::Slot ring[tk::kRingSlots];
   int ring_next = 0;
@@ -550,6 +551,7 @@ int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed
   inst->dec_ws_bytes = decode_attention_workspace_bytes(max_chunk, m.n_heads, m.head_dim,
                                                         std::min(inst->dec_max_ctx, 1 << 16));
   TK_CUDA(cudaMalloc(&inst->dec_ws, inst->dec_ws_bytes));
+  TK_CUDA(cudaMalloc(&inst->attn_partial, attn_partial_bytes(m.n_heads, m.head_dim)));
   for (auto& s : inst->ring) {
     TK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.host), kSlotBytes, cudaHostAllocDefault));
     TK_CUDA(cudaMalloc(&s.dev, kSlotBytes));
@@ -584,6 +586,7 @@ int tk_instance_destroy(tk_instance* inst) {
   cudaFree(inst->logits);
   cudaFree(inst->gemm_ws);
   cudaFree(inst->dec_ws);
+  cudaFree(inst->attn_partial);
   cudaStreamDestroy(inst->s_compute);
   cudaStreamDestroy(inst->s_copy);
   cudaStreamDestroy(inst->s_pred);
@@ -692,9 +695,17 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
   const int n_emit = static_cast<int>(emit_rows.size());
   int32_t* emit_d;
   pk.put(emit_rows.data(), n_emit, &emit_d);
+  const int qcap = n_slices + n_tokens / 128 + 1;
+  AttnQBlock* qb_d;
+  AttnQBlock* qbs = pk.put<AttnQBlock>(nullptr, qcap, &qb_d);
   AttnWork* work_d;
-  AttnWork* work = pk.put<AttnWork>(nullptr, n_tokens + n_slices, &work_d);
-  const int n_work = build_attn_work(slices, n_slices, work, n_tokens + n_slices);
+  AttnWork* work = pk.put<AttnWork>(nullptr, qcap + kAttnMaxSplitSlots, &work_d);
+  int n_qb = 0;
+  const int n_work = build_attn_work(slices, n_slices, m.n_heads, qbs, qcap, work,
+                                     qcap + kAttnMaxSplitSlots, &n_qb);
+  TK_CHECK(n_work >= 0, TK_EINVAL, "prefill: attention work list overflow");
+  bool any_split = false;
+  for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
   int32_t* out_d;
   int32_t* out_h = pk.put<int32_t>(nullptr, std::max(1, n_slices), &out_d);
   int32_t* tok_d;
@@ -722,7 +733,8 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
   for (int l = 0; l < m.n_layers; ++l) {
     rc = run_layer(inst, l, n_tokens, meta_d, s, attn_flops, attn_bytes, [&]() {
       return launch_chunk_attention_work(inst->qkv, 3 * h, inst->attn, inst->pool, inst->geom, l,
-                                         work_d, n_work, sl_d, bt_d, scale, s);
+                                         work_d, n_work, qb_d, n_qb, any_split, sl_d, bt_d, scale,
+                                         inst->attn_partial, s);
     });
     if (rc) return rc;
   }
@@ -1084,26 +1096,38 @@ int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_
   TK_CHECK(slices && block_tables && n_slices > 0, TK_EINVAL, "tk_chunk_attention: arguments");
   int n_bt = 0;
   for (int i = 0; i < n_slices; ++i) n_bt = std::max(n_bt, slices[i].bt_offset + slices[i].n_pages);
-  std::vector<AttnWork> work(n_tokens + n_slices);
-  const int n_work = build_attn_work(slices, n_slices, work.data(), static_cast<int>(work.size()));
+  const int qcap = n_slices + n_tokens / 128 + 1;
+  std::vector<AttnQBlock> qbs(qcap);
+  std::vector<AttnWork> work(qcap + kAttnMaxSplitSlots);
+  int n_qb = 0;
+  const int n_work = build_attn_work(slices, n_slices, n_heads, qbs.data(), qcap, work.data(),
+                                     static_cast<int>(work.size()), &n_qb);
   TK_CHECK(n_work >= 0, TK_EINVAL, "tk_chunk_attention: work list");
+  bool any_split = false;
+  for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  void *d_sl, *d_bt, *d_work;
+  void *d_sl, *d_bt, *d_work, *d_qb, *d_part;
   TK_CUDA(cudaMalloc(&d_sl, n_slices * sizeof(tk_slice)));
   TK_CUDA(cudaMalloc(&d_bt, std::max(1, n_bt) * 4));
   TK_CUDA(cudaMalloc(&d_work, std::max(1, n_work) * sizeof(AttnWork)));
+  TK_CUDA(cudaMalloc(&d_qb, std::max(1, n_qb) * sizeof(AttnQBlock)));
+  TK_CUDA(cudaMalloc(&d_part, attn_partial_bytes(n_heads, head_dim)));
   TK_CUDA(cudaMemcpy(d_sl, slices, n_slices * sizeof(tk_slice), cudaMemcpyHostToDevice));
   TK_CUDA(cudaMemcpy(d_bt, block_tables, n_bt * 4, cudaMemcpyHostToDevice));
   TK_CUDA(cudaMemcpy(d_work, work.data(), n_work * sizeof(AttnWork), cudaMemcpyHostToDevice));
+  TK_CUDA(cudaMemcpy(d_qb, qbs.data(), n_qb * sizeof(AttnQBlock), cudaMemcpyHostToDevice));
   KvGeom g{n_layers, n_heads, head_dim, page_tokens};
   int rc = launch_chunk_attention_work(
       static_cast<const __nv_bfloat16*>(q), q_stride, static_cast<__nv_bfloat16*>(o),
       static_cast<const __nv_bfloat16*>(kv_pool), g, layer, static_cast<AttnWork*>(d_work),
-      n_work, static_cast<tk_slice*>(d_sl), static_cast<int32_t*>(d_bt), scale, s);
+      n_work, static_cast<AttnQBlock*>(d_qb), n_qb, any_split, static_cast<tk_slice*>(d_sl),
+      static_cast<int32_t*>(d_bt), scale, static_cast<float*>(d_part), s);
   TK_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_sl);
   cudaFree(d_bt);
   cudaFree(d_work);
+  cudaFree(d_qb);
+  cudaFree(d_part);
   return rc;
 }
 

@@ -62,18 +62,31 @@ int launch_gather_rows_f32(const float* x, const int32_t* rows, int n, int cols,
 int launch_kv_write(__nv_bfloat16* qkv, const TokenMeta* meta, int n, __nv_bfloat16* pool,
                     KvGeom g, int layer, float q_scale, int rope, float rope_theta,
                     cudaStream_t s);
-struct AttnWork {
+// Chunk attention work decomposition (host-built, staged to the device).
+constexpr int kAttnMaxSplitSlots = 64;   // split partial buffers per launch
+constexpr int kAttnMinSplitBlocks = 8;   // >= 512 keys per KV split
+struct AttnQBlock {
   int32_t slice;
-  int32_t row0;   // chunk row of the first query of this 64-row block
-  int32_t nrows;  // <= 64
-  int32_t pos0;   // position of that query in its request
+  int32_t row0;        // chunk row of the first query of this <=128-row block
+  int32_t nrows;
+  int32_t pos0;        // position of that query in its request
+  int32_t n_splits;    // KV splits of this block (1: written directly)
+  int32_t first_slot;  // partial slot of split 0 when n_splits > 1
 };
-// Host: split each slice into <=64-row query blocks; returns count or -1.
-int build_attn_work(const tk_slice* slices, int n_slices, AttnWork* out, int cap);
+struct AttnWork {
+  int32_t qblock;
+  int32_t kb0, kb1;    // 64-key blocks [kb0, kb1)
+  int32_t slot;        // partial slot (-1: unsplit)
+};
+int build_attn_work(const tk_slice* slices, int n_slices, int n_heads, AttnQBlock* qbs, int qcap,
+                    AttnWork* items, int icap, int* n_qblocks);
+int64_t attn_partial_bytes(int n_heads, int head_dim);
 int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloat16* o,
                                 const __nv_bfloat16* pool, KvGeom g, int layer,
-                                const AttnWork* work, int n_work, const tk_slice* slices_dev,
-                                const int32_t* bt_dev, float scale, cudaStream_t s);
+                                const AttnWork* work, int n_work, const AttnQBlock* qblocks,
+                                int n_qblocks, bool any_split, const tk_slice* slices_dev,
+                                const int32_t* bt_dev, float scale, float* partial,
+                                cudaStream_t s);
 int64_t decode_attention_workspace_bytes(int batch, int n_heads, int head_dim, int max_ctx);
 int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16* o,
                             const __nv_bfloat16* pool,

@@ -161,3 +161,24 @@ def test_chunk_attention_mixed_slices():
         err = (o[row:row + n].float() - ref).abs().max().item()
         assert err < 2e-2, (s, n, err)
         row += n
+
+
+def test_gemm_shared_workspace_across_shapes():
+    """One workspace serves every GEMM shape of a layer (as in the runtime)."""
+    import ctypes
+    shapes = [(512, 15360, 5120), (512, 5120, 5120), (33, 20480, 5120), (512, 5120, 20480),
+              (7, 50272, 5120)]
+    need = 0
+    for M, N, K in shapes:
+        nb = ctypes.c_int64()
+        native.check(native.load().tk_gemm_workspace_bytes(M, N, K, ctypes.byref(nb)))
+        need = max(need, nb.value)
+    ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for _ in range(2):
+        for M, N, K in shapes:
+            a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+            b = (torch.randn(N, K, device="cuda", generator=g) * 0.02).bfloat16()
+            out = native.gemm(a, b, epilogue=native.EPI_F32, workspace=ws)
+            torch.cuda.synchronize()
+            assert _rel_err(out, a.float() @ b.float().t()) < 2e-3, (M, N, K)
