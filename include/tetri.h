@@ -142,7 +142,9 @@ int tk_host_free(void* p);
 
 /* --- events ----------------------------------------------------------------
  * tk_event_query: 1 done (host outputs written), 0 pending.  elapsed_ns is
- * the device time between the event's start and end markers.               */
+ * the device time between the event's start and end markers.
+ * tk_event_release: the handle is no longer used; if the work has not been
+ * observed complete yet, its host outputs are abandoned (never written).     */
 int tk_event_query(tk_event* ev, int64_t* elapsed_ns);
 int tk_event_wait(tk_event* ev, int64_t* elapsed_ns);
 int tk_event_release(tk_event* ev);

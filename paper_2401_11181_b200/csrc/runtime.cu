@@ -299,7 +299,8 @@ namespace tk {
 static int finalize_event(tk_event* ev) {
   if (ev->finished) return TK_OK;
   TK_CUDA(cudaEventSynchronize(ev->end));
-  if (ev->out_dst) {
+  // a released event abandons its host outputs (the caller's buffer may be gone)
+  if (ev->out_dst && !ev->released) {
     for (int i = 0; i < ev->n_out; ++i)
       ev->out_dst[i] = ev->remap ? (ev->remap[i] >= 0 ? ev->out_src[ev->remap[i]] : -1)
                                  : ev->out_src[i];
@@ -538,11 +539,17 @@ int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed
   TK_CUDA(cudaMalloc(&inst->ffn, rows * ffn_cols * 2));
   inst->max_emit = max_chunk;
   TK_CUDA(cudaMalloc(&inst->logits, rows * static_cast<int64_t>(inst->w->head_rows) * 4));
+  // The stream-K plan depends on M only through ceil(M/128): size the shared
+  // workspace for every row count a call may use.
   int64_t ws = 0;
-  for (int64_t n : {3LL * m.hidden, static_cast<long long>(m.hidden),
-                    static_cast<long long>(ffn_cols), static_cast<long long>(inst->w->head_rows)}) {
-    for (int64_t k : {static_cast<long long>(m.hidden), static_cast<long long>(m.ffn)})
-      ws = std::max(ws, gemm_workspace_bytes(max_chunk, n, k));
+  const int gate_up = m.arch == TK_ARCH_OPT ? m.ffn : 2 * m.ffn;
+  for (int rows_m = 128; rows_m < max_chunk + 128; rows_m += 128) {
+    const int mm = std::min(rows_m, max_chunk);
+    ws = std::max(ws, gemm_workspace_bytes(mm, 3 * m.hidden, m.hidden));
+    ws = std::max(ws, gemm_workspace_bytes(mm, m.hidden, m.hidden));
+    ws = std::max(ws, gemm_workspace_bytes(mm, gate_up, m.hidden));
+    ws = std::max(ws, gemm_workspace_bytes(mm, m.hidden, m.ffn));
+    ws = std::max(ws, gemm_workspace_bytes(mm, inst->w->head_rows, m.hidden));
   }
   inst->gemm_ws_bytes = ws;
   TK_CUDA(cudaMalloc(&inst->gemm_ws, ws));
@@ -568,10 +575,10 @@ int tk_instance_destroy(tk_instance* inst) {
   cudaSetDevice(inst->device);
   cudaDeviceSynchronize();
   for (auto& s : inst->ring) {
-    if (s.owner) {
-      finalize_event(s.owner);
-      s.owner->slot = nullptr;
-      maybe_free_event(s.owner);
+    if (tk_event* ev = s.owner) {
+      finalize_event(ev);  // clears s.owner
+      ev->slot = nullptr;
+      maybe_free_event(ev);
     }
     cudaFreeHost(s.host);
     cudaFree(s.dev);

@@ -1,0 +1,314 @@
+"""CUDA executor: the scheduler's decisions executed on B200s via libtetri.
+
+Each scheduler instance (p{i}, d{i}, c{i}) gets a device-side ``native.Instance``
+(weights shared per device/model/seed, its own page-major KV pool and streams).
+The executor keeps the *physical* side of the KV cache consistent with the
+scheduler's page *counts* (PagedKvStore, pdsim/decode.py:41-95):
+
+* prefill: a request's prompt pages are allocated from the prefill pool when
+  its first slice is scheduled (pdsim/prefill.py:355-357) and freed when its
+  KV handoff to the decode instance completes;
+* handoff (pdsim/prefill.py:420-424): ``tk_kv_send`` copies the prompt pages
+  page-by-page into pages of the destination pool (NVLink P2P across GPUs,
+  a device copy when co-located).  Pages of a request that has arrived but is
+  not yet admitted live in a receive staging area of the decode pool, outside
+  ``mem_capacity_tokens`` (SURVEY.md §7 "KV residency");
+* admission turns the staged pages into resident pages without a copy; next-
+  token growth allocates pages (pdsim/decode.py:298-311); swap-out copies the
+  victim's pages to pinned host memory and frees them (pdsim/decode.py:313-334);
+  swap-in restores them into freshly allocated pages;
+* a decode step feeds each running request its last token at position
+  ``kv_tokens`` (prompt + generated) in ``running`` order
+  (pdsim/decode.py:255-256) and keeps the greedy next tokens.
+
+Length predictor: buckets come from the statistical PredictorModel on the
+reference's "predictor" stream (decision parity; random-init weights carry no
+signal), while the OPT-125M-class classifier runs on the prefill GPU for its
+real cost -- concurrently on the predictor stream in ``parallel`` mode, before
+the round's first chunk in ``sequential`` mode (pdsim/prefill.py:338-346).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import costs, native
+from .engine import SimulationError
+from .workload import Request, token_ids_for
+
+
+@dataclass
+class _Pool:
+    """Physical page ids of one instance's KV pool."""
+
+    n_pages: int
+    free: list[int] = field(default_factory=list)
+
+    def __post_init__(self):
+        self.free = list(range(self.n_pages - 1, -1, -1))
+
+    def take(self, n: int, who: str) -> list[int]:
+        if n > len(self.free):
+            raise SimulationError(f"{who}: physical KV pool exhausted ({n} pages wanted, "
+                                  f"{len(self.free)} free of {self.n_pages})")
+        return [self.free.pop() for _ in range(n)]
+
+    def give(self, pages: list[int]) -> None:
+        self.free.extend(reversed(pages))
+
+
+class _Done:
+    """A completion handle that is already complete (no device work)."""
+
+    def done(self) -> bool:
+        return True
+
+
+class _Then:
+    """Device handle plus a host callback run once when it completes."""
+
+    def __init__(self, ev: native.Event, fn):
+        self.ev, self.fn, self.fired = ev, fn, False
+
+    def done(self) -> bool:
+        if self.ev.done():
+            if not self.fired:
+                self.fired = True
+                self.fn()
+            return True
+        return False
+
+    def wait(self):
+        self.ev.wait()
+        return self.done()
+
+
+class CudaExecutor:
+    """Executor protocol of executor.py on real devices."""
+
+    def __init__(self, config, requests: list[Request] | None = None):
+        native.load()
+        self.config = config
+        self.params = config.params
+        mcfg = dict(config.model)
+        self.shape = native.MODELS[mcfg.get("name", "opt-13b")]
+        self.seed = int(mcfg.get("seed", 0))
+        self.page_tokens = self.params.page_size
+        n_dev = native.device_count()
+        if n_dev < 1:
+            raise native.NativeError("CudaExecutor needs at least one CUDA device")
+        self.n_dev = n_dev
+        self.devices = dict(config.devices)
+        # pools (pages); defaults fit OPT-13B co-located on one 180 GB B200
+        self.prefill_pages = int(mcfg.get("prefill_pages", 2048))
+        self.staging_pages = int(mcfg.get("staging_pages", 512))
+        self.max_batch = int(mcfg.get("max_decode_batch", 256))
+        self.device_predictor = bool(mcfg.get("device_predictor", True))
+        self.insts: dict[str, native.Instance] = {}
+        self.pools: dict[str, _Pool] = {}
+        self.tables: dict[str, dict[int, list[int]]] = {}   # inst -> req -> pages
+        self.kv_home: dict[int, str] = {}                     # req -> instance holding its KV
+        self.first_token: dict[int, int] = {}
+        self.last_token: dict[int, int] = {}
+        self.swap_host: dict[int, tuple[int, int]] = {}       # req -> (pinned ptr, pages)
+        self.predictors: dict[int, native.Instance] = {}
+        self.prompts: dict[int, list[int]] = {}
+        self.stats = {"prefill_tokens": 0, "prefill_chunks": 0, "decode_steps": 0,
+                      "decode_tokens": 0, "kv_bytes_sent": 0, "prefill_device_ns": 0,
+                      "decode_device_ns": 0, "handoff_device_ns": 0, "predict_calls": 0}
+        self._req_by_id: dict[int, Request] = {r.id: r for r in (requests or [])}
+
+    # -- lifecycle ---------------------------------------------------------------------
+    def _device_of(self, iid: str) -> int:
+        if iid in self.devices:
+            return int(self.devices[iid]) % self.n_dev
+        kind, idx = iid[0], int(iid[1:])
+        if kind == "p" or kind == "c":
+            return idx % self.n_dev
+        return (self.config.n_prefill + idx) % self.n_dev
+
+    def attach(self, inst) -> None:
+        dev = self._device_of(inst.id)
+        if inst.role == "prefill":
+            pages, max_rows = self.prefill_pages, self.params.chunk_size
+        elif inst.role == "decode":
+            pages, max_rows = self.params.capacity_pages + self.staging_pages, self.max_batch
+        else:  # coupled: prefill + decode share one pool
+            pages = self.params.capacity_pages + self.staging_pages
+            max_rows = max(self.params.chunk_size, self.max_batch)
+        self.insts[inst.id] = native.Instance(self.shape, device=dev, seed=self.seed,
+                                              kv_pages=pages, page_tokens=self.page_tokens,
+                                              max_chunk=max_rows)
+        self.pools[inst.id] = _Pool(pages)
+        self.tables[inst.id] = {}
+        if inst.role == "prefill" and self.device_predictor and dev not in self.predictors:
+            self.predictors[dev] = native.Instance(native.PREDICTOR_125M, device=dev,
+                                                   seed=self.seed + 1, kv_pages=16 * 32 + 8,
+                                                   max_chunk=16 * 512)
+
+    def detach(self, inst) -> None:
+        pass  # device state is kept; flips reuse the id with a new role object
+
+    def close(self) -> None:
+        for i in list(self.insts.values()) + list(self.predictors.values()):
+            i.close()
+        for ptr, _ in self.swap_host.values():
+            native.host_free(ptr)
+        self.swap_host.clear()
+
+    def _ids(self, req: Request) -> list[int]:
+        ids = self.prompts.get(req.id)
+        if ids is None:
+            ids = self.prompts[req.id] = token_ids_for(req, self.shape.vocab, self.seed)
+        return ids
+
+    # -- prefill side -----------------------------------------------------------------------
+    def predict_round(self, inst, batch, predictor) -> object:
+        """Device classifier over the round's prompts (cost); buckets stay statistical."""
+        dev = self._device_of(inst.id)
+        pred = self.predictors.get(dev)
+        if pred is None or not batch:
+            return 0
+        max_len = 512
+        ids, lens = [], []
+        for r in batch:
+            toks = self._ids(r)[:max_len]
+            ids += toks
+            lens.append(len(toks))
+        ev, _ = pred.predict(ids, lens, max_len)
+        self.stats["predict_calls"] += 1
+        if predictor.mode == "sequential":
+            ev.wait()  # the round's first chunk starts after the predictor pass
+        return 0
+
+    def prefill_chunk(self, inst, chunk, starting: int, tax: bool, extra) -> object:
+        dev_inst = self.insts[inst.id]
+        pool = self.pools[inst.id]
+        tables = self.tables[inst.id]
+        ids, slices, bt = [], [], []
+        emit_rids = []
+        for rid, start, n in chunk.slices:
+            req = inst.requests[rid]
+            if start == 0:
+                tables[rid] = pool.take(costs.pages_needed(self.params, req.prompt_len), inst.id)
+                self.kv_home[rid] = inst.id
+            ids += self._ids(req)[start:start + n]
+            emit = int(start + n == req.prompt_len)
+            slices.append((start, n, len(bt), len(tables[rid]), emit))
+            bt += tables[rid]
+            if emit:
+                emit_rids.append((len(slices) - 1, rid))
+        ev, out = dev_inst.prefill_chunk(ids, slices, bt)
+        self.stats["prefill_tokens"] += len(ids)
+        self.stats["prefill_chunks"] += 1
+
+        def publish():
+            for idx, rid in emit_rids:
+                self.first_token[rid] = int(out[idx])
+                self.last_token[rid] = int(out[idx])
+            self.stats["prefill_device_ns"] += ev.elapsed_ns
+
+        return _Then(ev, publish)
+
+    def round_done(self, inst, requests) -> None:
+        pass
+
+    def kv_transfer(self, src_inst, req: Request, dst: str) -> object:
+        src_id = self.kv_home.get(req.id) if src_inst is None else src_inst.id
+        if src_id is None or req.id not in self.tables.get(src_id, {}):
+            raise SimulationError(f"request {req.id}: no KV to transfer")
+        src_pages = self.tables[src_id].pop(req.id)
+        dst_pages = self.pools[dst].take(len(src_pages), dst)  # receive staging
+        self.tables[dst][req.id] = dst_pages
+        self.kv_home[req.id] = dst
+        ev = self.insts[src_id].kv_send(src_pages, self.insts[dst], dst_pages)
+        nbytes = len(src_pages) * self.insts[src_id].page_bytes
+        self.stats["kv_bytes_sent"] += nbytes
+
+        def release_src():
+            self.pools[src_id].give(src_pages)
+            self.stats["handoff_device_ns"] += ev.elapsed_ns
+
+        return _Then(ev, release_src)
+
+    # -- decode side ----------------------------------------------------------------------------
+    def admit(self, inst, dreq) -> None:
+        # staged pages become resident pages: the counts check happened in the store
+        have = self.tables[inst.id].get(dreq.req.id)
+        need = costs.pages_needed(self.params, dreq.kv_tokens)
+        if have is None:
+            self.tables[inst.id][dreq.req.id] = self.pools[inst.id].take(need, inst.id)
+        elif len(have) < need:
+            have += self.pools[inst.id].take(need - len(have), inst.id)
+
+    def grow(self, inst, dreq, pages: int) -> None:
+        t = self.tables[inst.id][dreq.req.id]
+        if pages > len(t):
+            t += self.pools[inst.id].take(pages - len(t), inst.id)
+
+    def release(self, inst, dreq) -> None:
+        pages = self.tables[inst.id].pop(dreq.req.id, [])
+        self.pools[inst.id].give(pages)
+        self.kv_home.pop(dreq.req.id, None)
+
+    def swap_out(self, inst, dreq) -> None:
+        pages = self.tables[inst.id].pop(dreq.req.id)
+        dev = self.insts[inst.id]
+        ptr = native.host_alloc(len(pages) * dev.page_bytes)
+        dev.swap_out(pages, ptr).wait()  # pages are reused right away by the grower
+        self.swap_host[dreq.req.id] = (ptr, len(pages))
+        self.pools[inst.id].give(pages)
+
+    def swap_in(self, inst, dreq) -> None:
+        ptr, n = self.swap_host.pop(dreq.req.id)
+        pages = self.pools[inst.id].take(n, inst.id)
+        self.insts[inst.id].swap_in(pages, ptr).wait()
+        native.host_free(ptr)
+        self.tables[inst.id][dreq.req.id] = pages
+
+    def decode_step(self, inst, running, kv_tokens: int, swapped_out: int,
+                    swapped_in: int) -> tuple[object, int]:
+        p = inst.params
+        modeled = costs.decode_iter_latency(p, len(running), kv_tokens) \
+            + round(p.swap_penalty_us_per_page * (swapped_out + swapped_in))
+        dev = self.insts[inst.id]
+        tables = self.tables[inst.id]
+        stride = max(len(tables[d.req.id]) for d in running)
+        bt, last, ctx = [], [], []
+        for d in running:
+            t = tables[d.req.id]
+            bt += t + [t[0]] * (stride - len(t))
+            last.append(self.last_token.get(d.req.id, 0))
+            ctx.append(d.kv_tokens)
+        if len(running) > dev.max_chunk:
+            raise SimulationError(f"{inst.id}: decode batch {len(running)} exceeds the device "
+                                  f"batch capacity {dev.max_chunk}")
+        ev, out = dev.decode_step(last, ctx, bt, stride)
+        rids = [d.req.id for d in running]
+        self.stats["decode_steps"] += 1
+        self.stats["decode_tokens"] += len(rids)
+
+        def publish():
+            for i, rid in enumerate(rids):
+                self.last_token[rid] = int(out[i])
+            self.stats["decode_device_ns"] += ev.elapsed_ns
+
+        return _Then(ev, publish), modeled
+
+    def mixed_step(self, inst, prefilling, running, prefill_tokens, kv_tokens, swapped_out,
+                   swapped_in):
+        raise SimulationError("coupled instances on the CUDA executor are not supported yet "
+                              "(SURVEY.md §8(f) rank 1)")
+
+    # -- reporting ---------------------------------------------------------------------------------
+    def summary_extras(self) -> dict:
+        s = dict(self.stats)
+        s["model"] = self.shape.name
+        s["devices"] = {k: self._device_of(k) for k in self.insts}
+        if s["prefill_device_ns"]:
+            s["prefill_tok_s_device"] = s["prefill_tokens"] / (s["prefill_device_ns"] / 1e9)
+        if s["decode_device_ns"]:
+            s["decode_tok_s_device"] = s["decode_tokens"] / (s["decode_device_ns"] / 1e9)
+        if s["handoff_device_ns"]:
+            s["handoff_gb_s"] = s["kv_bytes_sent"] / s["handoff_device_ns"]
+        return s

@@ -1,0 +1,67 @@
+"""The unchanged scheduler driving real device work (executor="cuda").
+
+Checks conservation and causality of a measured-clock run (every request
+prefilled, handed off and decoded exactly as many steps as pdsim would run
+it), that the physical KV pages come back to the pools, and that the first
+scheduling round's chunk layout equals the simulated run's (it depends only
+on the burst, not on timing).
+"""
+
+import pytest
+
+import paper_2401_11181_b200 as tk
+from paper_2401_11181_b200.experiment import make_executor, run_experiment
+
+pytestmark = pytest.mark.gpu
+
+CFG = {
+    "cluster": {"prefill": 1, "decode": 1},
+    "workload": {"n_requests": 24, "mixture": {"LPLD": 0.5, "LPHD": 0.5},
+                 "lengths": {"heavy_decode": {"hi": 300}}},
+    "cost_model": {"preset": "nvlink300", "mem_capacity_tokens": 16000},
+    "model": {"name": "tiny", "prefill_pages": 1024, "staging_pages": 256,
+              "max_decode_batch": 64},
+}
+
+
+def test_cuda_executor_end_to_end():
+    cfg = tk.config_from_dict(dict(CFG, executor="cuda"))
+    res = run_experiment(cfg, seed=0)
+    s = res.summary
+    assert s["completed"] == s["n_requests"] == 24
+    for row in res.rows:
+        assert 0 <= row["wait_us"] <= row["ttft_us"] <= row["jct_us"]
+    dev = s["device"]
+    reqs = tk.generate(cfg.workload_spec, tk.RngStreams(0).stream("workload"))
+    assert dev["prefill_tokens"] == sum(r.prompt_len for r in reqs)
+    assert dev["decode_tokens"] == sum(r.true_decode_len for r in reqs)
+    assert dev["kv_bytes_sent"] == sum(
+        -(-r.prompt_len // 16) for r in reqs) * 16 * 2 * 2 * 256 * 2  # pages x page bytes
+    assert dev["predict_calls"] >= 1
+    # the first round's chunk layout does not depend on timing
+    sim = run_experiment(tk.config_from_dict(CFG), seed=0)
+    n = len(sim.control.instances["p0"].chunk_log)
+    first_sim = [c[1:] for c in sim.control.instances["p0"].chunk_log][: min(n, 3)]
+    first_dev = [c[1:] for c in res.control.instances["p0"].chunk_log][: len(first_sim)]
+    assert first_dev == first_sim
+
+
+def test_cuda_executor_greedy_swaps_restore_pages():
+    cfg = tk.config_from_dict({
+        "executor": "cuda",
+        "workload": {"class": "LPLD", "n_requests": 6, "lengths": {
+            "light_prompt": {"median": 16, "sigma": 0.0, "lo": 16, "hi": 16},
+            "light_decode": {"median": 64, "sigma": 0.0, "lo": 64, "hi": 64}}},
+        "policies": {"prefill": "fcfs", "decode": "greedy"},
+        "predictor": {"granularity": 16, "accuracy": 1.0},
+        "cost_model": {"mem_capacity_tokens": 320, "preset": "nvlink300"},
+        "model": {"name": "tiny", "prefill_pages": 64, "staging_pages": 64,
+                  "max_decode_batch": 16},
+    })
+    executor = make_executor(cfg)
+    res = run_experiment(cfg, seed=5, executor=executor)
+    assert res.summary["completed"] == 6
+    assert res.summary["swap_events_total"] > 0
+    # every physical page is back in its pool
+    for iid, pool in executor.pools.items():
+        assert len(pool.free) == pool.n_pages, iid
