@@ -370,8 +370,10 @@ def run_ours(args, world, rank, local):
                     for k, v in prof.items()},
         "clocks": clk,
     }
-    line["share_of_step"] = {k: round(v["ms"] / (dev_s * 1e3 / world * world), 4)
-                             for k, v in prof.items()}
+    line["share_of_step"] = {k: round(v["ms"] / (dev_s * 1e3), 4) for k, v in prof.items()}
+    inst.close()
+    if world == 1 and not args.no_serving:
+        line["serving"] = serving_run(args)
     if world == 1 and not args.no_cpu_baseline:
         all_chunks = [(p[1], p[3]) for plan in plans for p in plan]
         pick = [all_chunks[int(i * len(all_chunks) / 6)] for i in range(6)]
@@ -379,6 +381,36 @@ def run_ours(args, world, rank, local):
         line["cpu_baseline"] = {"value": round(tok_s, 3), "unit": "tok/s", "cores": cores,
                                 "kind": "port", "sample": desc}
     print(json.dumps(line))
+
+
+def serving_run(args) -> dict:
+    """Mixed workload through the reference scheduler + CUDA executor (measured clock)."""
+    import paper_2401_11181_b200 as tk
+    from paper_2401_11181_b200.experiment import run_experiment
+    cfg = {"cluster": {"prefill": 1, "decode": 1},
+           "workload": {"n_requests": args.serving_n},
+           "cost_model": {"preset": "nvlink300", "mem_capacity_tokens": 40000},
+           "model": {"name": args.model, "prefill_pages": 2048, "staging_pages": 512,
+                     "max_decode_batch": 256, "seed": args.seed}}
+    sim = run_experiment(tk.config_from_dict(cfg), seed=args.seed).summary
+    res = run_experiment(tk.config_from_dict(dict(cfg, executor="cuda")), seed=args.seed)
+    s, d = res.summary, res.summary["device"]
+    return {
+        "workload": f"Mixed-{args.serving_n} (four-class, burst), 1 prefill + 1 decode instance "
+                    f"co-located on one GPU, {args.model}, reserve_dynamic, power-of-two, "
+                    "predictor g=200 p=0.749 (device classifier for cost)",
+        "ttft_avg_ms": round(s["ttft"]["avg_us"] / 1e3, 2),
+        "jct_avg_ms": round(s["jct"]["avg_us"] / 1e3, 2),
+        "ttft_p99_ms": round(s["ttft"]["p99_us"] / 1e3, 2),
+        "jct_p99_ms": round(s["jct"]["p99_us"] / 1e3, 2),
+        "prefill_tok_s": round(d.get("prefill_tok_s_device", 0.0), 1),
+        "decode_tok_s": round(d.get("decode_tok_s_device", 0.0), 1),
+        "kv_handoff_gb_s": round(d.get("handoff_gb_s", 0.0), 1),
+        "makespan_s": round(s["makespan_us"] / 1e6, 3),
+        "reference_modeled": {"ttft_avg_ms": round(sim["ttft"]["avg_us"] / 1e3, 2),
+                              "jct_avg_ms": round(sim["jct"]["avg_us"] / 1e3, 2),
+                              "note": "pdsim cost model (V100-calibrated), same workload"},
+    }
 
 
 def main():
@@ -391,6 +423,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-serving", action="store_true")
+    ap.add_argument("--serving-n", type=int, default=32)
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -34,6 +34,7 @@
 #include "tk_kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace tk {
 
@@ -101,16 +102,21 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& p, int row, int c
   }
   if constexpr (EPI == EPI_F32_BIAS_RESID || EPI == EPI_F32) {
     float* out = reinterpret_cast<float*>(p.C) + static_cast<size_t>(row) * p.N + col0;
+    if constexpr (EPI == EPI_F32_BIAS_RESID) {
+      float4 r[8];  // loads first: no store may sit between them
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        if (col0 + g * 4 < p.N) r[g] = __ldcg(reinterpret_cast<const float4*>(out + g * 4));
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        v[g * 4] += r[g].x; v[g * 4 + 1] += r[g].y; v[g * 4 + 2] += r[g].z; v[g * 4 + 3] += r[g].w;
+      }
+    }
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
-      if (col0 + g * 4 < p.N) {
-        float4 o = make_float4(v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]);
-        if constexpr (EPI == EPI_F32_BIAS_RESID) {
-          float4 r = *reinterpret_cast<float4*>(out + g * 4);
-          o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
-        }
-        *reinterpret_cast<float4*>(out + g * 4) = o;
-      }
+      if (col0 + g * 4 < p.N)
+        *reinterpret_cast<float4*>(out + g * 4) =
+            make_float4(v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]);
     }
   } else {
     __nv_bfloat16* out =
@@ -371,6 +377,521 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
+
+// ============================================================================
+// Skinny GEMM for decode-sized M (<= 128 rows): swap A/B so the weight tile is
+// the 128-row UMMA operand and the batch is the UMMA N (NB = 16..128).
+//   D^T[n, m] = W[n, :] . X[m, :]      (TMEM: 128 lanes = output features,
+//                                        NB columns = batch rows)
+// The kernel is weight-streaming (HBM) bound: 8..12 TMA stages of 16 KB weight
+// tiles per SM keep ~150 KB in flight per SM; stream-K over (n-tile, k-block)
+// keeps every SM streaming; partial tiles are only 128 x NB fp32.
+template <int NB>
+struct SkinnyCfg {
+  static constexpr int BM = 128;  // weight rows per tile
+  static constexpr int BK = 64;
+  static constexpr int W_BYTES = BM * BK * 2;
+  static constexpr int X_BYTES = NB * BK * 2;
+  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 12 ? 12 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (2 * NB < 32) ? 32 : 2 * NB;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
+  static constexpr int THREADS = 192;
+};
+
+template <int NB, int EPI>
+__device__ __forceinline__ void skinny_store(const GemmArgs& p, int n, int m0, const float* v,
+                                             int count) {
+  // v[j] = D[n, m0 + j]: output feature n of batch row m0 + j
+  if (n >= p.N) return;
+  float b = 0.f;
+  if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_RELU || EPI == EPI_F32_BIAS_RESID) {
+    if (p.bias != nullptr) b = __bfloat162float(p.bias[n]);
+  }
+  const int rows = min(count, p.M - m0);
+  if constexpr (EPI == EPI_F32_BIAS_RESID) {
+    // all residual loads first (independent), then the stores
+    float* c = reinterpret_cast<float*>(p.C) + static_cast<size_t>(m0) * p.N + n;
+    float r[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < rows) r[j] = __ldcg(c + static_cast<size_t>(j) * p.N);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < rows) c[static_cast<size_t>(j) * p.N] = r[j] + v[j] + b;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j >= rows) break;
+      float x = v[j] + b;
+      if constexpr (EPI == EPI_BF16_BIAS_RELU) x = fmaxf(x, 0.f);
+      const size_t off = static_cast<size_t>(m0 + j) * p.N + n;
+      if constexpr (EPI == EPI_F32) reinterpret_cast<float*>(p.C)[off] = x;
+      else reinterpret_cast<__nv_bfloat16*>(p.C)[off] = __float2bfloat16(x);
+    }
+  }
+}
+
+template <int NB, int EPI>
+__global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
+    gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmap_w,
+                       const __grid_constant__ CUtensorMap tmap_x, const GemmArgs p) {
+  using Cfg = SkinnyCfg<NB>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sw = smem;
+  uint8_t* sx = smem + Cfg::STAGES * Cfg::W_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const long long T = p.total_iters;
+  const int G = gridDim.x;
+  const long long it_begin = static_cast<long long>(blockIdx.x) * T / G;
+  const long long it_end = static_cast<long long>(blockIdx.x + 1) * T / G;
+  const int kbs = p.kbs;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = l2_policy_evict_first();
+      const uint64_t pol_x = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long i = it_begin; i < it_end;) {
+        const int tile = static_cast<int>(i / kbs);
+        const long long seg_end = min(it_end, static_cast<long long>(tile + 1) * kbs);
+        for (int kb = static_cast<int>(i - static_cast<long long>(tile) * kbs);
+             kb < static_cast<int>(seg_end - static_cast<long long>(tile) * kbs); ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sw + stage * Cfg::W_BYTES, &tmap_w, &full[stage], kb * Cfg::BK,
+                      tile * Cfg::BM, pol_w);
+          tma_load_2d(sx + stage * Cfg::X_BYTES, &tmap_x, &full[stage], kb * Cfg::BK, 0, pol_x);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        i = seg_end;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(Cfg::BM, NB);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (long long i = it_begin; i < it_end;) {
+        const int tile = static_cast<int>(i / kbs);
+        const long long seg_end = min(it_end, static_cast<long long>(tile + 1) * kbs);
+        const int nkb = static_cast<int>(seg_end - i);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * NB;
+        for (int k = 0; k < nkb; ++k) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t w_addr = smem_u32(sw + stage * Cfg::W_BYTES);
+          const uint32_t x_addr = smem_u32(sx + stage * Cfg::X_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < Cfg::BK / 16; ++kk)
+            umma_bf16(d_tmem, umma_desc_sw128(w_addr + kk * 32), umma_desc_sw128(x_addr + kk * 32),
+                      idesc, (k > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        i = seg_end;
+      }
+    }
+  } else {
+    const uint32_t quarter = warp & 3;
+    const int feat_in_tile = static_cast<int>(quarter * 32 + lane);
+    const bool leader = (warp == 2 && lane == 0);
+    const int tid_e = static_cast<int>(threadIdx.x) - 64;
+    constexpr int CH = NB >= 32 ? 32 : NB;  // columns per TMEM load
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long i = it_begin; i < it_end;) {
+      const int tile = static_cast<int>(i / kbs);
+      const long long tile_first = static_cast<long long>(tile) * kbs;
+      const long long seg_end = min(it_end, tile_first + kbs);
+      const int n = tile * Cfg::BM + feat_in_tile;
+      const int contrib = owner_of(tile_first + kbs - 1, T, G) - owner_of(tile_first, T, G) + 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((quarter * 32) << 16) + acc * NB;
+      if (contrib == 1) {
+#pragma unroll 1
+        for (int c = 0; c < NB / CH; ++c) {
+          uint32_t r[32];
+          if constexpr (CH == 32) tmem_ld_32x32b_x32(t_row + c * CH, *reinterpret_cast<uint32_t(*)[32]>(r));
+          else tmem_ld_32x32b_x16(t_row + c * CH, r);
+          tmem_wait_ld();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(r[j]);
+          skinny_store<NB, EPI>(p, n, c * CH, v, CH);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else {
+        int* counter = p.counters + tile;
+        int* flags = p.counters + p.tiles_n + static_cast<size_t>(tile) * p.slots;
+        if (leader) *last_flag = atomicAdd(counter, 1);
+        named_bar_sync(1, 128);
+        const int arrival = *last_flag;
+        const size_t slot_elems = static_cast<size_t>(NB) * 128;
+        float* tile_ws = p.ws + static_cast<size_t>(tile) * p.slots * slot_elems;
+        if (arrival < contrib - 1) {
+          float* mine = tile_ws + static_cast<size_t>(arrival) * slot_elems;
+#pragma unroll 1
+          for (int c = 0; c < NB / CH; ++c) {
+            uint32_t r[32];
+            if constexpr (CH == 32) tmem_ld_32x32b_x32(t_row + c * CH, *reinterpret_cast<uint32_t(*)[32]>(r));
+            else tmem_ld_32x32b_x16(t_row + c * CH, r);
+            tmem_wait_ld();
+            float4* dst = reinterpret_cast<float4*>(mine + (static_cast<size_t>(c) * 128 + tid_e) * CH);
+#pragma unroll
+            for (int g = 0; g < CH / 4; ++g)
+              __stcg(dst + g, make_float4(__uint_as_float(r[g * 4]), __uint_as_float(r[g * 4 + 1]),
+                                          __uint_as_float(r[g * 4 + 2]), __uint_as_float(r[g * 4 + 3])));
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (leader) st_release(flags + arrival, 1);
+        } else {
+          if (leader) {
+            for (int a = 0; a < contrib - 1; ++a)
+              while (ld_acquire(flags + a) == 0) {
+              }
+          }
+          named_bar_sync(1, 128);
+          __threadfence();
+#pragma unroll 1
+          for (int c = 0; c < NB / CH; ++c) {
+            uint32_t r[32];
+            if constexpr (CH == 32) tmem_ld_32x32b_x32(t_row + c * CH, *reinterpret_cast<uint32_t(*)[32]>(r));
+            else tmem_ld_32x32b_x16(t_row + c * CH, r);
+            tmem_wait_ld();
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(r[j]);
+            for (int a = 0; a < contrib - 1; ++a) {
+              const float4* src = reinterpret_cast<const float4*>(
+                  tile_ws + static_cast<size_t>(a) * slot_elems + (static_cast<size_t>(c) * 128 + tid_e) * CH);
+#pragma unroll
+              for (int g = 0; g < CH / 4; ++g) {
+                const float4 t = __ldcg(src + g);
+                v[g * 4] += t.x; v[g * 4 + 1] += t.y; v[g * 4 + 2] += t.z; v[g * 4 + 3] += t.w;
+              }
+            }
+            skinny_store<NB, EPI>(p, n, c * CH, v, CH);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          named_bar_sync(1, 128);
+          if (leader) {
+            for (int a = 0; a < contrib - 1; ++a) flags[a] = 0;
+            *counter = 0;
+          }
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      i = seg_end;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+}
+
+
+// ============================================================================
+// CTA-pair GEMM (tcgen05.mma.cta_group::2): a pair of CTAs on one TPC computes
+// a 256 x 256 tile; each CTA holds 128 rows of A and 128 rows (half) of the
+// B tile, the leader (even) CTA issues UMMA M=256 N=256 that reads both CTAs'
+// shared memory and accumulates into both CTAs' TMEM (128 lanes x 256 cols
+// each).  Per SM and k-block this moves 32 KB into shared memory for the
+// same MMA work the 1-CTA kernel needs 48 KB for, which removes its
+// shared-memory-bandwidth ceiling.  With CS = 4 two pairs (two 256-row
+// m-groups) form a cluster and every B half is loaded as two 64-row slices
+// multicast to the CTAs of both pairs that hold that half, so weights are
+// still fetched once per GEMM.
+template <int EPI, int CS>
+__global__ void __launch_bounds__(192, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                     const __grid_constant__ CUtensorMap tmap_b, const GemmArgs p) {
+  constexpr int BM = 128, BN = 256, BK = 64;
+  constexpr int STAGES = 6;
+  constexpr int A_BYTES = BM * BK * 2;        // own 128 rows
+  constexpr int BH_BYTES = (BN / 2) * BK * 2;  // own half of the B tile
+  constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
+  constexpr int PAIR_STAGE_BYTES = 2 * STAGE_BYTES;
+  constexpr int NPAIRS = CS / 2;
+  constexpr int SLICE_ROWS = (BN / 2) / NPAIRS;  // B-half rows each CTA loads
+  constexpr int SLICE_BYTES = SLICE_ROWS * BK * 2;
+  constexpr int TMEM_COLS = 512;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int rank = static_cast<int>(cluster_ctarank());
+  const int pair = rank >> 1;
+  const int half = rank & 1;
+  const bool leader = half == 0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);        // leader: its expect_tx arrive (+ all TMA bytes of the pair)
+      mbar_init(&empty[s], NPAIRS);  // one MMA-commit arrive per pair reading this stage
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int cluster = blockIdx.x / CS;
+  const int G = gridDim.x / CS;
+  const int groups_m = p.tiles_m / CS;  // 128-row m-tiles per cluster m-group = CS
+  const long long T = p.total_iters;
+  const long long it_begin = static_cast<long long>(cluster) * T / G;
+  const long long it_end = static_cast<long long>(cluster + 1) * T / G;
+  const int kbs = p.kbs;
+  const uint16_t all_mask = static_cast<uint16_t>((1u << CS) - 1);
+  const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * pair));
+  // CTAs holding this CTA's B half in any pair: ranks {half, half+2, ...}
+  const uint16_t half_mask = static_cast<uint16_t>(CS == 4 ? ((1u << half) | (1u << (half + 2)))
+                                                           : (1u << half));
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_a = l2_policy_evict_last();
+      const uint64_t pol_b = l2_policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long i = it_begin; i < it_end;) {
+        const int ctile = static_cast<int>(i / kbs);
+        const long long seg_end = min(it_end, static_cast<long long>(ctile + 1) * kbs);
+        const int m_idx = (ctile % groups_m) * CS + rank;  // this CTA's 128-row tile
+        const int n_idx = ctile / groups_m;
+        for (int kb = static_cast<int>(i - static_cast<long long>(ctile) * kbs);
+             kb < static_cast<int>(seg_end - static_cast<long long>(ctile) * kbs); ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], PAIR_STAGE_BYTES);
+          tma_load_2d_pair(sa + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, m_idx * BM,
+                           pol_a);
+          const int brow = n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS;
+          uint8_t* bdst = sb + stage * BH_BYTES + pair * SLICE_BYTES;
+          if constexpr (CS == 2)
+            tma_load_2d_pair(bdst, &tmap_b, &full[stage], kb * BK, brow, pol_b);
+          else
+            tma_load_2d_pair_mc(bdst, &tmap_b, &full[stage], kb * BK, brow, half_mask, pol_b);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        i = seg_end;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (long long i = it_begin; i < it_end;) {
+        const int ctile = static_cast<int>(i / kbs);
+        const long long seg_end = min(it_end, static_cast<long long>(ctile + 1) * kbs);
+        const int nkb = static_cast<int>(seg_end - i);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int k = 0; k < nkb; ++k) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sa + stage * A_BYTES);
+          const uint32_t b_addr = smem_u32(sb + stage * BH_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16_pair(d_tmem, umma_desc_sw128(a_addr + kk * 32),
+                           umma_desc_sw128(b_addr + kk * 32), idesc, (k > 0 || kk > 0) ? 1u : 0u);
+          umma_commit_pair_mc(&empty[stage], all_mask);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair_mc(&tfull[acc], pair_mask);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        i = seg_end;
+      }
+    }
+  } else {
+    const uint32_t quarter = warp & 3;
+    const int row_in_tile = static_cast<int>(quarter * 32 + lane);
+    const bool ep_leader = (warp == 2 && lane == 0);
+    const int tid_e = static_cast<int>(threadIdx.x) - 64;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long i = it_begin; i < it_end;) {
+      const int ctile = static_cast<int>(i / kbs);
+      const long long tile_first = static_cast<long long>(ctile) * kbs;
+      const long long seg_end = min(it_end, tile_first + kbs);
+      const int m_idx = (ctile % groups_m) * CS + rank;
+      const int n_idx = ctile / groups_m;
+      const int tile = n_idx * p.tiles_m + m_idx;
+      const int row = m_idx * BM + row_in_tile;
+      const int col_base = n_idx * BN;
+      const int contrib = owner_of(tile_first + kbs - 1, T, G) - owner_of(tile_first, T, G) + 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((quarter * 32) << 16) + acc * BN;
+      auto release_tmem = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      };
+      if (contrib == 1) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, r);
+          tmem_wait_ld();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          epilogue_store<EPI>(p, row, col_base + c * 32, v);
+        }
+        release_tmem();
+      } else {
+        int* counter = p.counters + tile;
+        int* flags = p.counters + p.tiles_m * p.tiles_n + static_cast<size_t>(tile) * p.slots;
+        if (ep_leader) *last_flag = atomicAdd(counter, 1);
+        named_bar_sync(1, 128);
+        const int arrival = *last_flag;
+        const size_t slot_elems = static_cast<size_t>(BN / 32) * 128 * 32;
+        float* tile_ws = p.ws + static_cast<size_t>(tile) * p.slots * slot_elems;
+        if (arrival < contrib - 1) {
+          float* mine = tile_ws + static_cast<size_t>(arrival) * slot_elems;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_row + c * 32, r);
+            tmem_wait_ld();
+            float4* dst = reinterpret_cast<float4*>(mine + (static_cast<size_t>(c) * 128 + tid_e) * 32);
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              __stcg(dst + g, make_float4(__uint_as_float(r[g * 4]), __uint_as_float(r[g * 4 + 1]),
+                                          __uint_as_float(r[g * 4 + 2]), __uint_as_float(r[g * 4 + 3])));
+          }
+          release_tmem();
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (ep_leader) st_release(flags + arrival, 1);
+        } else {
+          if (ep_leader) {
+            for (int a = 0; a < contrib - 1; ++a)
+              while (ld_acquire(flags + a) == 0) {
+              }
+          }
+          named_bar_sync(1, 128);
+          __threadfence();
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_row + c * 32, r);
+            tmem_wait_ld();
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            for (int a = 0; a < contrib - 1; ++a) {
+              const float4* src = reinterpret_cast<const float4*>(
+                  tile_ws + static_cast<size_t>(a) * slot_elems + (static_cast<size_t>(c) * 128 + tid_e) * 32);
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const float4 t = __ldcg(src + g);
+                v[g * 4] += t.x; v[g * 4 + 1] += t.y; v[g * 4 + 2] += t.z; v[g * 4 + 3] += t.w;
+              }
+            }
+            epilogue_store<EPI>(p, row, col_base + c * 32, v);
+          }
+          release_tmem();
+          named_bar_sync(1, 128);
+          if (ep_leader) {
+            for (int a = 0; a < contrib - 1; ++a) flags[a] = 0;
+            *counter = 0;
+          }
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      i = seg_end;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+}
+
+constexpr int kPairSmemBytes = 6 * (128 * 64 * 2 + 128 * 64 * 2) + 256 + 1024;
+
 // ------------------------------------------------------------------ host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -419,22 +940,61 @@ static int max_clusters_for(int bn, int cs);
 // partial slots of any shape: it has a fixed size.
 constexpr int64_t kCounterBytes = 1 << 20;
 
+constexpr int kSkinnyMaxM = 128;
+
+static int skinny_nb(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128; }
+
 struct GemmPlan {
   bool counters_fit;
+  bool pair;    // cta_group::2 path (tiles_m even)
+  bool skinny;  // swap-AB weight-streaming path (M <= 128)
+  int nb;       // skinny: UMMA N (batch rows, padded)
   int bn, cs, tiles_m, tiles_n, kbs, clusters, slots;
   long long total_iters;
   int64_t ws_bytes;
 };
 
+static int max_skinny_ctas(int nb);
+static int max_pair_clusters(int cs);
+
+static GemmPlan plan_skinny(int M, int N, int K, int max_ctas) {
+  GemmPlan pl{};
+  pl.skinny = true;
+  pl.nb = skinny_nb(M);
+  pl.bn = 128;
+  pl.cs = 1;
+  pl.tiles_m = 1;
+  pl.tiles_n = (N + 127) / 128;
+  pl.kbs = K / 64;
+  pl.total_iters = static_cast<long long>(pl.tiles_n) * pl.kbs;
+  int ctas = max_skinny_ctas(pl.nb);
+  if (max_ctas > 0) ctas = std::min(ctas, max_ctas);
+  ctas = static_cast<int>(std::min<long long>(ctas, std::max<long long>(1, pl.total_iters / 4)));
+  pl.clusters = ctas;
+  int most = 1;
+  for (long long t = 0; t < pl.tiles_n; ++t) {
+    const int c = owner_of((t + 1) * pl.kbs - 1, pl.total_iters, ctas) -
+                  owner_of(t * pl.kbs, pl.total_iters, ctas) + 1;
+    most = std::max(most, c);
+  }
+  pl.slots = most - 1;
+  pl.ws_bytes = kCounterBytes + static_cast<int64_t>(pl.tiles_n) * pl.slots * 128LL * pl.nb * 4;
+  pl.counters_fit = static_cast<int64_t>(pl.tiles_n) * (1 + pl.slots) * 4 <= kCounterBytes;
+  return pl;
+}
+
 static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
+  if (M <= kSkinnyMaxM && getenv("TK_NO_SKINNY") == nullptr) return plan_skinny(M, N, K, max_ctas);
   GemmPlan pl{};
   pl.bn = pick_bn(N);
   pl.tiles_m = (M + 127) / 128;
+  pl.pair = pl.bn == 256 && pl.tiles_m % 2 == 0 && getenv("TK_NO_PAIR") == nullptr;
   pl.tiles_n = (N + pl.bn - 1) / pl.bn;
   pl.kbs = K / 64;
   pl.cs = pl.tiles_m % 4 == 0 ? 4 : (pl.tiles_m % 2 == 0 ? 2 : 1);
   pl.total_iters = static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
-  int clusters = max_clusters_for(pl.bn, pl.cs);
+  if (pl.pair && pl.cs == 1) pl.cs = 2;
+  int clusters = pl.pair ? max_pair_clusters(pl.cs) : max_clusters_for(pl.bn, pl.cs);
   if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / pl.cs));
   clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, pl.total_iters / 4)));
   pl.clusters = clusters;
@@ -455,6 +1015,120 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
 }
 
 int64_t gemm_workspace_bytes(int M, int N, int K) { return plan_gemm(M, N, K, 0).ws_bytes; }
+
+template <int NB, int EPI>
+static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& a,
+                         int ctas, cudaStream_t stream) {
+  using Cfg = SkinnyCfg<NB>;
+  auto kern = gemm_skinny_kernel<NB, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM_BYTES));
+    configured = true;
+  }
+  kern<<<ctas, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tw, tx, a);
+  TK_CUDA(cudaGetLastError());
+  note_launch();
+  return TK_OK;
+}
+
+template <int NB>
+static int skinny_epi(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& a, int ctas,
+                      cudaStream_t s) {
+  switch (a.epi) {
+    case EPI_BF16: return launch_skinny<NB, EPI_BF16>(tw, tx, a, ctas, s);
+    case EPI_BF16_BIAS: return launch_skinny<NB, EPI_BF16_BIAS>(tw, tx, a, ctas, s);
+    case EPI_BF16_BIAS_RELU: return launch_skinny<NB, EPI_BF16_BIAS_RELU>(tw, tx, a, ctas, s);
+    case EPI_F32_BIAS_RESID: return launch_skinny<NB, EPI_F32_BIAS_RESID>(tw, tx, a, ctas, s);
+    case EPI_F32: return launch_skinny<NB, EPI_F32>(tw, tx, a, ctas, s);
+  }
+  set_error("unknown gemm epilogue");
+  return TK_EINVAL;
+}
+
+template <int EPI, int CS>
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                       int clusters, cudaStream_t stream) {
+  auto kern = gemm_pair_kernel<EPI, CS>;
+  static bool configured = false;
+  if (!configured) {
+    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kPairSmemBytes));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * CS);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = kPairSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
+  note_launch();
+  return TK_OK;
+}
+
+template <int CS>
+static int pair_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int clusters,
+                    cudaStream_t s) {
+  switch (a.epi) {
+    case EPI_BF16: return launch_pair<EPI_BF16, CS>(ta, tb, a, clusters, s);
+    case EPI_BF16_BIAS: return launch_pair<EPI_BF16_BIAS, CS>(ta, tb, a, clusters, s);
+    case EPI_BF16_BIAS_RELU: return launch_pair<EPI_BF16_BIAS_RELU, CS>(ta, tb, a, clusters, s);
+    case EPI_F32_BIAS_RESID: return launch_pair<EPI_F32_BIAS_RESID, CS>(ta, tb, a, clusters, s);
+    case EPI_F32: return launch_pair<EPI_F32, CS>(ta, tb, a, clusters, s);
+  }
+  set_error("unknown gemm epilogue");
+  return TK_EINVAL;
+}
+
+template <int CS>
+static int query_pair_clusters() {
+  auto kern = gemm_pair_kernel<EPI_BF16, CS>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmemBytes) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return kNumSMs / CS;
+  }
+  cudaLaunchConfig_t q{};
+  q.gridDim = dim3(kNumSMs / CS * CS);
+  q.blockDim = dim3(192);
+  q.dynamicSmemBytes = kPairSmemBytes;
+  cudaLaunchAttribute qa[1];
+  qa[0].id = cudaLaunchAttributeClusterDimension;
+  qa[0].val.clusterDim.x = CS;
+  qa[0].val.clusterDim.y = 1;
+  qa[0].val.clusterDim.z = 1;
+  q.attrs = qa;
+  q.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return kNumSMs / CS;
+  }
+  return n;
+}
+
+static int max_pair_clusters(int cs) {
+  static int c2 = 0, c4 = 0;
+  if (cs == 4) {
+    if (!c4) c4 = query_pair_clusters<4>();
+    return c4;
+  }
+  if (!c2) c2 = query_pair_clusters<2>();
+  return c2;
+}
+
+static int max_skinny_ctas(int nb) {
+  (void)nb;
+  return kNumSMs;  // one CTA per SM (>100 KB of smem each)
+}
 
 template <int BN, int EPI, int CS>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
@@ -558,6 +1232,34 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   const GemmPlan pl = plan_gemm(M, N, K, max_ctas);
   TK_CHECK(ws_bytes >= pl.ws_bytes, TK_EINVAL, "gemm: workspace too small");
   TK_CHECK(pl.counters_fit, TK_EINVAL, "gemm: too many tiles for the counter region");
+  if (pl.skinny) {
+    CUtensorMap tw, tx;
+    int rc = make_tmap_kmajor(&tw, B, N, K, 128);
+    if (rc) return rc;
+    rc = make_tmap_kmajor(&tx, A, M, K, pl.nb);
+    if (rc) return rc;
+    GemmArgs a{};
+    a.C = C;
+    a.bias = static_cast<const __nv_bfloat16*>(bias);
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.epi = epi;
+    a.tiles_m = 1;
+    a.tiles_n = pl.tiles_n;
+    a.kbs = pl.kbs;
+    a.cs = 1;
+    a.slots = pl.slots;
+    a.total_iters = pl.total_iters;
+    a.counters = static_cast<int*>(workspace);
+    a.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
+    switch (pl.nb) {
+      case 16: return skinny_epi<16>(tw, tx, a, pl.clusters, stream);
+      case 32: return skinny_epi<32>(tw, tx, a, pl.clusters, stream);
+      case 64: return skinny_epi<64>(tw, tx, a, pl.clusters, stream);
+      default: return skinny_epi<128>(tw, tx, a, pl.clusters, stream);
+    }
+  }
   CUtensorMap ta;
   int rc = make_tmap_kmajor(&ta, A, M, K, 128);
   if (rc) return rc;
@@ -578,6 +1280,14 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   (void)tiles;
   a.counters = static_cast<int*>(workspace);
   a.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
+  if (pl.pair) {
+    // each CTA loads 64-row (CS=4) or 128-row (CS=2) slices of its B half
+    CUtensorMap tb;
+    rc = make_tmap_kmajor(&tb, B, N, K, 128 / (pl.cs / 2));
+    if (rc) return rc;
+    if (pl.cs == 4) return pair_epi<4>(ta, tb, a, pl.clusters, stream);
+    return pair_epi<2>(ta, tb, a, pl.clusters, stream);
+  }
   if (pl.bn == 256) return dispatch_cs<256>(B, N, K, ta, a, pl.clusters, stream);
   return dispatch_cs<128>(B, N, K, ta, a, pl.clusters, stream);
 }

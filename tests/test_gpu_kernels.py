@@ -36,6 +36,10 @@ def _rel_err(x, ref):
     (256, 5120, 5120),   # 2-CTA cluster multicast
     (1024, 3072, 768),   # two m-groups of a 4-CTA cluster
     (384, 2048, 1024),   # tiles_m=3 -> no cluster
+    (1, 5120, 5120),     # skinny (swap-AB) path: single decode row
+    (16, 5120, 20480),   # skinny NB=16, long K (many stream-K contributors)
+    (100, 20480, 5120),  # skinny NB=128
+    (128, 15360, 5120),  # skinny at the M boundary
 ])
 def test_gemm_matches_fp32(M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
@@ -51,8 +55,9 @@ def test_gemm_matches_fp32(M, N, K):
     assert _rel_err(out2, ref2) < 1e-2
 
 
-def test_gemm_residual_epilogue_and_workspace_reuse():
-    M, N, K = 512, 5120, 20480  # FC2 shape; several CTAs share each tile
+@pytest.mark.parametrize("M", [512, 32])
+def test_gemm_residual_epilogue_and_workspace_reuse(M):
+    N, K = 5120, 20480  # FC2 shape; several CTAs share each tile
     g = torch.Generator(device="cuda").manual_seed(1)
     a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     b = (torch.randn(N, K, device="cuda", generator=g) * 0.02).bfloat16()
