@@ -283,8 +283,13 @@ def run_ours(args, world, rank, local):
     def run_round(plan):
         evs, toks = [], 0
         h2d = d2h = 0
-        for ids, slices, bt, real in plan:
+        verbose = os.environ.get("TK_BENCH_VERBOSE")
+        for ci, (ids, slices, bt, real) in enumerate(plan):
             ev, out = inst.prefill_chunk(ids, slices, bt)
+            if verbose:
+                ev.wait()
+                print(f"chunk {ci} slices={[(s[0], s[1]) for s in slices]} "
+                      f"{ev.elapsed_ns / 1e6:.2f} ms", file=sys.stderr, flush=True)
             a, b = inst.staged_bytes()
             h2d, d2h = h2d + a, d2h + b
             evs.append((ev, out))
@@ -414,6 +419,9 @@ def serving_run(args) -> dict:
 
 
 def main():
+    if os.environ.get("TK_BENCH_WATCHDOG"):
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["TK_BENCH_WATCHDOG"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=4)

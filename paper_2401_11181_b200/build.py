@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libtetri.so"
 INCLUDE = PKG.parent / "include"
-SOURCES = ["gemm.cu", "kernels.cu", "runtime.cu"]
+SOURCES = ["gemm.cu", "kernels.cu", "attention_tc.cu", "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          f"-I{INCLUDE}", f"-I{CSRC}"]

@@ -462,10 +462,10 @@ __global__ void __launch_bounds__(kAttnThreads)
             pack_bf16x2(acc[nt][2] * inv_hi, acc[nt][3] * inv_hi);
     }
   } else {
-    // partial[(slot * H + head) * 128 + row][D + 2]: O unnormalised, m, l
-    float* base = partial + (static_cast<size_t>(w.slot) * g.n_heads + head) * kAttnRows * (D + 2);
-    float* plo = base + static_cast<size_t>(r_lo) * (D + 2);
-    float* phi = base + static_cast<size_t>(r_hi) * (D + 2);
+    // partial[(slot * H + head) * 128 + row][D + 4]: O unnormalised, m, l
+    float* base = partial + (static_cast<size_t>(w.slot) * g.n_heads + head) * kAttnRows * (D + 4);
+    float* plo = base + static_cast<size_t>(r_lo) * (D + 4);
+    float* phi = base + static_cast<size_t>(r_hi) * (D + 4);
 #pragma unroll
     for (int nt = 0; nt < D / 8; ++nt) {
       *reinterpret_cast<float2*>(plo + nt * 8 + tq * 2) = make_float2(acc[nt][0], acc[nt][1]);
@@ -490,9 +490,9 @@ __global__ void __launch_bounds__(kAttnRows)
   const int head = blockIdx.y;
   const int row = threadIdx.x;
   if (row >= qb.nrows) return;
-  const size_t stride_slot = static_cast<size_t>(n_heads) * kAttnRows * (D + 2);
-  const float* first = partial + (static_cast<size_t>(qb.first_slot) * n_heads + head) * kAttnRows * (D + 2) +
-                       static_cast<size_t>(row) * (D + 2);
+  const size_t stride_slot = static_cast<size_t>(n_heads) * kAttnRows * (D + 4);
+  const float* first = partial + (static_cast<size_t>(qb.first_slot) * n_heads + head) * kAttnRows * (D + 4) +
+                       static_cast<size_t>(row) * (D + 4);
   float M = -INFINITY;
   for (int s = 0; s < qb.n_splits; ++s) M = fmaxf(M, first[s * stride_slot + D]);
   float L = 0.f;
@@ -516,14 +516,15 @@ __global__ void __launch_bounds__(kAttnRows)
 }
 
 int64_t attn_partial_bytes(int n_heads, int head_dim) {
-  return static_cast<int64_t>(kAttnMaxSplitSlots) * n_heads * kAttnRows * (head_dim + 2) * 4;
+  return static_cast<int64_t>(kAttnMaxSplitSlots) * n_heads * kAttnRows * (head_dim + 4) * 4;
 }
 
 // Host: slices -> 128-row q-blocks -> KV splits.  Splits are made only when the
 // grid would otherwise be small (target ~4 CTAs per SM including heads) and
 // never below kAttnMinSplitBlocks blocks of keys per split.
 int build_attn_work(const tk_slice* slices, int n_slices, int n_heads, AttnQBlock* qbs,
-                    int qcap, AttnWork* items, int icap, int* n_qblocks) {
+                    int qcap, AttnWork* items, int icap, int* n_qblocks, int block_keys) {
+  const int kAttnBlock = block_keys;  // keys per KV block of the consuming kernel
   int nq = 0, row = 0;
   int64_t total_blocks = 0;
   for (int i = 0; i < n_slices; ++i) {
@@ -549,7 +550,7 @@ int build_attn_work(const tk_slice* slices, int n_slices, int n_heads, AttnQBloc
     if (static_cast<int64_t>(nq) * n_heads < target_ctas) {
       const int64_t want = (target_ctas + static_cast<int64_t>(nq) * n_heads - 1) /
                            (static_cast<int64_t>(nq) * n_heads);
-      splits = static_cast<int>(std::min<int64_t>(want, nb / kAttnMinSplitBlocks));
+      splits = static_cast<int>(std::min<int64_t>(want, nb * block_keys / (64 * kAttnMinSplitBlocks)));
       splits = std::max(1, std::min(splits, 16));
       if (slot + splits > kAttnMaxSplitSlots) splits = 1;
     }
@@ -596,12 +597,7 @@ int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloa
                                                             scale_log2, partial);
     TK_CUDA(cudaGetLastError());
     note_launch();
-    if (any_split) {
-      attn_combine_kernel<128><<<dim3(n_qblocks, g.n_heads), kAttnRows, 0, s>>>(
-          o, qblocks, g.n_heads, partial);
-      TK_CUDA(cudaGetLastError());
-      note_launch();
-    }
+    if (any_split) return launch_attn_combine(o, qblocks, n_qblocks, g.n_heads, 128, partial, s);
   } else {
     const int smem = 4 * kAttnBlock * 64 * 2;
     chunk_attn_kernel<64><<<grid, kAttnThreads, smem, s>>>(q, q_stride, o, pool, g, layer, work,
@@ -609,13 +605,21 @@ int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloa
                                                            scale_log2, partial);
     TK_CUDA(cudaGetLastError());
     note_launch();
-    if (any_split) {
-      attn_combine_kernel<64><<<dim3(n_qblocks, g.n_heads), kAttnRows, 0, s>>>(
-          o, qblocks, g.n_heads, partial);
-      TK_CUDA(cudaGetLastError());
-      note_launch();
-    }
+    if (any_split) return launch_attn_combine(o, qblocks, n_qblocks, g.n_heads, 64, partial, s);
   }
+  return TK_OK;
+}
+
+int launch_attn_combine(__nv_bfloat16* o, const AttnQBlock* qblocks, int n_qblocks, int n_heads,
+                        int head_dim, float* partial, cudaStream_t s) {
+  if (head_dim == 128)
+    attn_combine_kernel<128><<<dim3(n_qblocks, n_heads), kAttnRows, 0, s>>>(o, qblocks, n_heads,
+                                                                            partial);
+  else
+    attn_combine_kernel<64><<<dim3(n_qblocks, n_heads), kAttnRows, 0, s>>>(o, qblocks, n_heads,
+                                                                           partial);
+  TK_CUDA(cudaGetLastError());
+  note_launch();
   return TK_OK;
 }
 

@@ -9,6 +9,7 @@
 // single H2D copy.  Every data-path call is asynchronous and returns a
 // tk_event whose completion also publishes the call's small host outputs.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -25,6 +26,11 @@
 namespace tk {
 
 static thread_local std::string g_err;
+
+bool use_tc_attention(int head_dim) {
+  static const bool forced_off = getenv("TK_ATTN_MMA_SYNC") != nullptr;
+  return head_dim == 128 && !forced_off;
+}
 static std::atomic<int64_t> g_launches{0};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -525,7 +531,11 @@ int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed
   inst->kv_pages = kv_pages;
   inst->page_bytes = static_cast<int64_t>(inst->geom.page_elems()) * 2;
   inst->max_chunk = max_chunk;
-  if (kv_pages > 0) TK_CUDA(cudaMalloc(&inst->pool, inst->page_bytes * kv_pages));
+  if (kv_pages > 0) {
+    TK_CUDA(cudaMalloc(&inst->pool, inst->page_bytes * kv_pages));
+    // stale slots are read (and masked) by whole-page loads: keep them finite
+    TK_CUDA(cudaMemset(inst->pool, 0, inst->page_bytes * kv_pages));
+  }
   TK_CUDA(cudaStreamCreateWithFlags(&inst->s_compute, cudaStreamNonBlocking));
   TK_CUDA(cudaStreamCreateWithFlags(&inst->s_copy, cudaStreamNonBlocking));
   TK_CUDA(cudaStreamCreateWithFlags(&inst->s_pred, cudaStreamNonBlocking));
@@ -708,8 +718,9 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
   AttnWork* work_d;
   AttnWork* work = pk.put<AttnWork>(nullptr, qcap + kAttnMaxSplitSlots, &work_d);
   int n_qb = 0;
+  const bool tc_attn = use_tc_attention(m.head_dim);
   const int n_work = build_attn_work(slices, n_slices, m.n_heads, qbs, qcap, work,
-                                     qcap + kAttnMaxSplitSlots, &n_qb);
+                                     qcap + kAttnMaxSplitSlots, &n_qb, tc_attn ? 128 : 64);
   TK_CHECK(n_work >= 0, TK_EINVAL, "prefill: attention work list overflow");
   bool any_split = false;
   for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
@@ -739,6 +750,10 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
   const double attn_bytes = 2.0 * m.hidden * 2 * prefix_tokens + 2.0 * n_tokens * m.hidden * 2;
   for (int l = 0; l < m.n_layers; ++l) {
     rc = run_layer(inst, l, n_tokens, meta_d, s, attn_flops, attn_bytes, [&]() {
+      if (tc_attn)
+        return launch_chunk_attention_tc(inst->qkv, inst->max_chunk, 3 * h, inst->attn, inst->pool,
+                                         inst->kv_pages, inst->geom, l, work_d, n_work, qb_d, n_qb,
+                                         any_split, sl_d, bt_d, scale, inst->attn_partial, s);
       return launch_chunk_attention_work(inst->qkv, 3 * h, inst->attn, inst->pool, inst->geom, l,
                                          work_d, n_work, qb_d, n_qb, any_split, sl_d, bt_d, scale,
                                          inst->attn_partial, s);
@@ -1107,8 +1122,9 @@ int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_
   std::vector<AttnQBlock> qbs(qcap);
   std::vector<AttnWork> work(qcap + kAttnMaxSplitSlots);
   int n_qb = 0;
+  const bool tc_attn = use_tc_attention(head_dim);
   const int n_work = build_attn_work(slices, n_slices, n_heads, qbs.data(), qcap, work.data(),
-                                     static_cast<int>(work.size()), &n_qb);
+                                     static_cast<int>(work.size()), &n_qb, tc_attn ? 128 : 64);
   TK_CHECK(n_work >= 0, TK_EINVAL, "tk_chunk_attention: work list");
   bool any_split = false;
   for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
@@ -1124,11 +1140,24 @@ int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_
   TK_CUDA(cudaMemcpy(d_work, work.data(), n_work * sizeof(AttnWork), cudaMemcpyHostToDevice));
   TK_CUDA(cudaMemcpy(d_qb, qbs.data(), n_qb * sizeof(AttnQBlock), cudaMemcpyHostToDevice));
   KvGeom g{n_layers, n_heads, head_dim, page_tokens};
-  int rc = launch_chunk_attention_work(
-      static_cast<const __nv_bfloat16*>(q), q_stride, static_cast<__nv_bfloat16*>(o),
-      static_cast<const __nv_bfloat16*>(kv_pool), g, layer, static_cast<AttnWork*>(d_work),
-      n_work, static_cast<AttnQBlock*>(d_qb), n_qb, any_split, static_cast<tk_slice*>(d_sl),
-      static_cast<int32_t*>(d_bt), scale, static_cast<float*>(d_part), s);
+  int rc;
+  if (tc_attn) {
+    // the pool extent: enough pages to cover every page id referenced
+    int max_page = 0;
+    for (int i = 0; i < n_bt; ++i) max_page = std::max(max_page, block_tables[i]);
+    rc = launch_chunk_attention_tc(
+        static_cast<const __nv_bfloat16*>(q), n_tokens, q_stride, static_cast<__nv_bfloat16*>(o),
+        static_cast<const __nv_bfloat16*>(kv_pool), max_page + 1, g, layer,
+        static_cast<AttnWork*>(d_work), n_work, static_cast<AttnQBlock*>(d_qb), n_qb, any_split,
+        static_cast<tk_slice*>(d_sl), static_cast<int32_t*>(d_bt), scale,
+        static_cast<float*>(d_part), s);
+  } else {
+    rc = launch_chunk_attention_work(
+        static_cast<const __nv_bfloat16*>(q), q_stride, static_cast<__nv_bfloat16*>(o),
+        static_cast<const __nv_bfloat16*>(kv_pool), g, layer, static_cast<AttnWork*>(d_work),
+        n_work, static_cast<AttnQBlock*>(d_qb), n_qb, any_split, static_cast<tk_slice*>(d_sl),
+        static_cast<int32_t*>(d_bt), scale, static_cast<float*>(d_part), s);
+  }
   TK_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_sl);
   cudaFree(d_bt);

@@ -79,7 +79,18 @@ struct AttnWork {
   int32_t slot;        // partial slot (-1: unsplit)
 };
 int build_attn_work(const tk_slice* slices, int n_slices, int n_heads, AttnQBlock* qbs, int qcap,
-                    AttnWork* items, int icap, int* n_qblocks);
+                    AttnWork* items, int icap, int* n_qblocks, int block_keys);
+int launch_attn_combine(__nv_bfloat16* o, const AttnQBlock* qblocks, int n_qblocks, int n_heads,
+                        int head_dim, float* partial, cudaStream_t s);
+// tcgen05 / TMEM chunk attention (head_dim 128, 128-key blocks).
+int launch_chunk_attention_tc(const __nv_bfloat16* qkv, int q_rows, int q_stride,
+                              __nv_bfloat16* o, const __nv_bfloat16* pool, int pool_pages,
+                              KvGeom g, int layer, const AttnWork* work, int n_work,
+                              const AttnQBlock* qblocks, int n_qblocks, bool any_split,
+                              const tk_slice* slices_dev, const int32_t* bt_dev, float scale,
+                              float* partial, cudaStream_t s);
+// true: use the tcgen05 attention for this head_dim (TK_ATTN_MMA_SYNC=1 forces mma.sync)
+bool use_tc_attention(int head_dim);
 int64_t attn_partial_bytes(int n_heads, int head_dim);
 int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloat16* o,
                                 const __nv_bfloat16* pool, KvGeom g, int layer,
