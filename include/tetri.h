@@ -85,7 +85,7 @@ int tk_device_count(int32_t* n);
 /* --- instances ------------------------------------------------------------
  * An instance = model weights (shared by every instance of the same model
  * and seed on one device) + a KV page pool of kv_pages pages of page_tokens
- * tokens in page-major layout [page][layer][K|V][head][page_tokens][head_dim]
+ * tokens in page-major layout [page][layer][head][K|V][page_tokens][head_dim]
  * bf16 + streams (compute, copy, predictor) + pinned staging.
  * max_chunk bounds tokens per tk_prefill_chunk / rows per tk_decode_step.   */
 int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed,

@@ -5,8 +5,10 @@
 // warps 0-3 with one query row per thread straight out of TMEM (no shuffles),
 // P (bf16) written to shared memory in the UMMA K-major SW128 layout,
 // O += P V  (UMMA, V as an MN-major operand -> TMEM).  K and V tiles are
-// TMA-loaded page by page from the page-major KV pool (16-token pages are
-// 2 KB-aligned [16][64] boxes per head-dim half), double buffered.
+// TMA-loaded from the page-major KV pool by 16 lanes of the producer warp in
+// parallel (2 KB [16 keys][64 d] boxes into [d-half][64 keys][128 B] tiles),
+// 64-key blocks in a 4-stage ring so three blocks are in flight ahead of the
+// tensor core; V is consumed as an MN-major operand.
 //
 // Warp roles (192 threads): 0-3 softmax / O correction / output, 4 TMA
 // producer, 5 TMEM allocator + single-thread UMMA issuer.  The issuer runs
@@ -18,17 +20,42 @@
 #include "tk_common.cuh"
 #include "tk_kernels.h"
 
+#include <cstdlib>
+
 namespace tk {
 
 namespace {
 constexpr int kRows = 128;
-constexpr int kKeys = 128;
+constexpr int kKeys = 64;                  // keys per KV block
 constexpr int kD = 128;
-constexpr int kTile = kRows * kD * 2;     // 32 KB: two SW128 atom columns of [128][64]
-constexpr int kHalf = kTile / 2;          // 16 KB: one atom column
-constexpr int kSmem = kTile * 6 + 1024 + 256;  // Q, K[2], V[2], P + barriers + align
+constexpr int kStages = 4;                 // K/V blocks in flight
+constexpr int kQTile = kRows * kD * 2;     // 32 KB: Q as two SW128 atom columns [128][64]
+constexpr int kQHalf = kQTile / 2;
+constexpr int kKvHalf = kKeys * 64 * 2;    // 8 KB: one d-half of a K or V block
+constexpr int kKTile = 2 * kKvHalf;        // 16 KB: [half][64 keys][128 B]
+constexpr int kStageBytes = 2 * kKTile;    // K then V
+constexpr int kPTile = kRows * kKeys * 2;  // 16 KB: P [128][64] bf16 (one atom column)
+constexpr int kSmem = kQTile + kStages * kStageBytes + 2 * kPTile + 1024 + 256;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
 }  // namespace
+
+// 2^x on the FMA/ALU pipes (no MUFU): x = n + f with |f| <= 1/2 by the
+// magic-constant rounding trick, 2^f by a degree-5 polynomial, 2^n added to
+// the exponent field with an integer add.  -inf maps to 2^-126 ~ 0.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  // round-to-nearest split via the 1.5 * 2^23 magic constant: x = n + f, |f| <= 1/2
+  const float y = x + 12582912.f;
+  const float n = y - 12582912.f;
+  const float f = x - n;
+  float q = 1.3333558e-3f;  // 2^f, degree-5 Taylor in f*ln2 (rel. err < 3e-6 on [-1/2,1/2])
+  q = fmaf(q, f, 9.6181291e-3f);
+  q = fmaf(q, f, 5.5504109e-2f);
+  q = fmaf(q, f, 2.4022651e-1f);
+  q = fmaf(q, f, 6.9314718e-1f);
+  q = fmaf(q, f, 1.0f);
+  return __int_as_float(__float_as_int(q) + ((__float_as_int(y) - 0x4B400000) << 23));
+}
 
 struct TcAttnParams {
   const AttnWork* work;
@@ -43,23 +70,22 @@ struct TcAttnParams {
 
 __global__ void __launch_bounds__(192, 1)
     chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                         const __grid_constant__ CUtensorMap tmap_kv, const TcAttnParams p) {
+                         const __grid_constant__ CUtensorMap tmap_k, const TcAttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + kTile;          // [2]
-  uint8_t* sV = smem + 3 * kTile;      // [2]
-  uint8_t* sP = smem + 5 * kTile;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * kTile);
+  uint8_t* sKV = smem + kQTile;                           // [stage]{K [half][64][128 B], V same}
+  uint8_t* sP = sKV + kStages * kStageBytes;              // [2][128][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPTile);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* s_free = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_done = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* kv_full = bars + 1;               // [kStages]
+  uint64_t* kv_empty = kv_full + kStages;     // [kStages]
+  uint64_t* s_full = kv_empty + kStages;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* p_full = s_free + 1;   // [2] per P buffer
+  uint64_t* o_done = p_full + 2;   // [2] per P buffer: PV_j retired (j % 2)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const AttnWork w = p.work[blockIdx.x];
@@ -72,16 +98,18 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 4 && lane == 0) {
     tma_prefetch_desc(&tmap_q);
-    tma_prefetch_desc(&tmap_kv);
+    tma_prefetch_desc(&tmap_k);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(s_free, 4);
-    mbar_init(p_full, 4);
-    mbar_init(o_done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&p_full[b], 4);
+      mbar_init(&o_done[b], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc<256>(tmem_slot);
@@ -91,30 +119,30 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = *tmem_slot;  // S at col 0, O at col 128
 
   if (warp == 4) {
+    // ------------------------------------------------------------ producer warp
+    // lane 0 owns the barriers; lanes 0-15 each issue one 2 KB box per block:
+    // lanes 0-7 K (page i, d-half h), lanes 8-15 V, into [half][64 keys][128 B].
+    const uint64_t pol = l2_policy_evict_first();
     if (lane == 0) {
-      // ------------------------------------------------------------ producer
-      const uint64_t pol = l2_policy_evict_first();
-      mbar_expect_tx(q_full, kTile);
+      mbar_expect_tx(q_full, kQTile);
       for (int h = 0; h < 2; ++h)
-        tma_load_2d(sQ + h * kHalf, &tmap_q, q_full, head * kD + h * 64, qb.row0, pol);
-      const int pt = p.page_tokens;
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * kTile);
-        const int first_page = (w.kb0 + j) * kKeys / pt;
-        for (int i = 0; i < kKeys / pt; ++i) {
-          const int pi = first_page + i;
-          const int page = pi < sl.n_pages ? pages[pi] : pages[0];  // beyond: masked
-          const int row_k = (((page * p.n_layers + p.layer) * 2 + 0) * p.n_heads + head) * pt;
-          const int row_v = row_k + p.n_heads * pt;
-          for (int h = 0; h < 2; ++h) {
-            tma_load_2d(sK + st * kTile + h * kHalf + i * pt * 128, &tmap_kv, &kv_full[st],
-                        h * 64, row_k, pol);
-            tma_load_2d(sV + st * kTile + h * kHalf + i * pt * 128, &tmap_kv, &kv_full[st],
-                        h * 64, row_v, pol);
-          }
-        }
+        tma_load_2d(sQ + h * kQHalf, &tmap_q, q_full, head * kD + h * 64, qb.row0, pol);
+    }
+    const int pt = p.page_tokens;
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j % kStages;
+      if (lane == 0) {
+        mbar_wait(&kv_empty[st], ((j / kStages) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], kStageBytes);
+      }
+      __syncwarp();
+      if (lane < 16) {
+        const int kv = lane >> 3, i = (lane >> 1) & 3, h = lane & 1;
+        const int pi = (w.kb0 + j) * kKeys / pt + i;
+        const int page = pi < sl.n_pages ? pages[pi] : pages[0];  // beyond: masked
+        const int blk = ((page * p.n_layers + p.layer) * p.n_heads + head) * 2 + kv;
+        tma_load_2d(sKV + st * kStageBytes + kv * kKTile + h * kKvHalf + i * pt * 128, &tmap_k,
+                    &kv_full[st], h * 64, blk * pt, pol);
       }
     }
   } else if (warp == 5) {
@@ -124,18 +152,17 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t idesc_pv = umma_idesc_bf16(kRows, kD) | (1u << 16);  // B MN-major
       mbar_wait(q_full, 0);
       tc_fence_after();
-      const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
+      const uint32_t q_addr = smem_u32(sQ);
       auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        const int st = j % kStages;
+        mbar_wait(&kv_full[st], (j / kStages) & 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + st * kTile);
+        const uint32_t k_addr = smem_u32(sKV + st * kStageBytes);
 #pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-          umma_bf16(tmem, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_s,
+        for (int kk = 0; kk < kD / 16; ++kk)
+          umma_bf16(tmem, umma_desc_sw128(q_addr + (kk >> 2) * kQHalf + (kk & 3) * 32),
+                    umma_desc_sw128(k_addr + (kk >> 2) * kKvHalf + (kk & 3) * 32), idesc_s,
                     kk > 0 ? 1u : 0u);
-        }
         umma_commit(s_full);
       };
       issue_s(0);
@@ -144,18 +171,18 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(s_free, j & 1);  // S_j is in the softmax warps' registers
           issue_s(j + 1);
         }
-        mbar_wait(p_full, j & 1);
+        const int pb = j & 1;
+        mbar_wait(&p_full[pb], (j >> 1) & 1);
         tc_fence_after();
-        const int st = j & 1;
-        const uint32_t v_addr = smem_u32(sV + st * kTile);
+        const int st = j % kStages;
+        const uint32_t v_addr = smem_u32(sKV + st * kStageBytes + kKTile);
+        const uint32_t p_addr = smem_u32(sP + pb * kPTile);
 #pragma unroll
-        for (int kk = 0; kk < kKeys / 16; ++kk) {
-          const uint32_t a_off = (kk >> 2) * kHalf + (kk & 3) * 32;  // P: K = keys
-          umma_bf16(tmem + kKeys, umma_desc_sw128(p_addr + a_off),
-                    umma_desc_sw128_mn(v_addr + kk * 2048, kHalf, 1024), idesc_pv,
+        for (int kk = 0; kk < kKeys / 16; ++kk)  // V: MN-major, d-halves 8 KB apart
+          umma_bf16(tmem + kKeys, umma_desc_sw128(p_addr + kk * 32),
+                    umma_desc_sw128_mn(v_addr + kk * 2048, kKvHalf, 1024), idesc_pv,
                     (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        umma_commit(o_done);
+        umma_commit(&o_done[pb]);
         umma_commit(&kv_empty[st]);
       }
     }
@@ -182,13 +209,20 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) mbar_arrive(s_free);
       const int k0 = (w.kb0 + j) * kKeys;
       const int lim = min(qp, kv_end - 1);  // last key this row may see
-      float mx = -INFINITY;
+      // Blocks entirely below every row's diagonal need no mask (warp-uniform).
+      const bool full = __all_sync(0xffffffffu, k0 + kKeys - 1 <= lim);
+      float raw_mx = -INFINITY;
+      if (full) {
 #pragma unroll
-      for (int c = 0; c < kKeys; ++c) {
-        const float v = (k0 + c <= lim) ? s[c] * p.scale_log2 : -INFINITY;
-        s[c] = v;
-        mx = fmaxf(mx, v);
+        for (int c = 0; c < kKeys; ++c) raw_mx = fmaxf(raw_mx, s[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < kKeys; ++c) {
+          s[c] = (k0 + c <= lim) ? s[c] : -INFINITY;
+          raw_mx = fmaxf(raw_mx, s[c]);
+        }
       }
+      const float mx = raw_mx * p.scale_log2;  // scale > 0: max commutes
       float corr = 1.f;
       bool rescale = false;
       if (mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx != -INFINITY)) {
@@ -198,20 +232,21 @@ __global__ void __launch_bounds__(192, 1)
       }
       l *= corr;
       const float base = (m_used == -INFINITY) ? 0.f : m_used;
-      // P_{j-1} is still being read by PV_{j-1} and O is being written: wait
-      if (j > 0) {
-        mbar_wait(o_done, (j - 1) & 1);
+      // P is double buffered: P_j's buffer was last read by PV_{j-2}
+      if (j > 1) {
+        mbar_wait(&o_done[j & 1], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
       }
-      uint8_t* prow = sP + r * 128;
+      uint8_t* prow = sP + (j & 1) * kPTile + r * 128;
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
+      for (int a = 0; a < kKeys / 64; ++a) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           float e[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
-            e[t] = exp2f(s[a * 64 + c * 8 + t] - base);
+            const float x = fmaf(s[a * 64 + c * 8 + t], p.scale_log2, -base);
+            e[t] = (c & 1) ? exp2_poly(x) : exp2f(x);  // FMA pipe / MUFU split
             l += e[t];
           }
           uint4 pk;
@@ -219,12 +254,15 @@ __global__ void __launch_bounds__(192, 1)
           pk.y = pack_bf16x2(e[2], e[3]);
           pk.z = pack_bf16x2(e[4], e[5]);
           pk.w = pack_bf16x2(e[6], e[7]);
-          *reinterpret_cast<uint4*>(prow + a * kHalf + ((c ^ (r & 7)) << 4)) = pk;
+          *reinterpret_cast<uint4*>(prow + a * kPTile + ((c ^ (r & 7)) << 4)) = pk;
         }
       }
       // tcgen05.ld/st are warp-collective: rescale if any row of the warp needs it
       // (rows that do not need it multiply by corr == 1)
       if (__any_sync(0xffffffffu, rescale && j > 0)) {
+        // O must hold PV_{j-1} before it is rescaled
+        mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < kD / 32; ++c) {
           uint32_t u[32];
@@ -239,10 +277,10 @@ __global__ void __launch_bounds__(192, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
     }
     // final O row
-    mbar_wait(o_done, (nblk - 1) & 1);
+    mbar_wait(&o_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     tc_fence_after();
     const int HD = p.n_heads * kD;
     if (qb.n_splits == 1) {
@@ -291,6 +329,7 @@ __global__ void __launch_bounds__(192, 1)
 
 int make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                      uint32_t box_rows);
+int make_tmap_kv_pages(CUtensorMap* map, const void* pool, uint64_t blocks, uint32_t page_tokens);
 
 // Q rows live in the fused qkv buffer: a [rows, row_elems] map, 128 x 64 boxes.
 static int make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint64_t row_elems,
@@ -305,14 +344,13 @@ int launch_chunk_attention_tc(const __nv_bfloat16* qkv, int q_rows, int q_stride
                               const tk_slice* slices_dev, const int32_t* bt_dev, float scale,
                               float* partial, cudaStream_t s) {
   TK_CHECK(g.head_dim == kD, TK_EUNSUPPORTED, "tcgen05 attention: head_dim 128");
-  TK_CHECK(kKeys % g.page_tokens == 0, TK_EUNSUPPORTED, "tcgen05 attention: page size");
+  TK_CHECK(g.page_tokens == 16, TK_EUNSUPPORTED, "tcgen05 attention: 16-token pages");
   if (n_work == 0) return TK_OK;
-  CUtensorMap tq, tkv;
+  CUtensorMap tq, tk;
   int rc = make_tmap_rows(&tq, qkv, q_rows, q_stride, kRows);
   if (rc) return rc;
-  const uint64_t pool_rows =
-      static_cast<uint64_t>(pool_pages) * g.n_layers * 2 * g.n_heads * g.page_tokens;
-  rc = make_tmap_rows(&tkv, pool, pool_rows, kD, g.page_tokens);
+  const uint64_t blocks = static_cast<uint64_t>(pool_pages) * g.n_layers * g.n_heads * 2;
+  rc = make_tmap_rows(&tk, pool, blocks * g.page_tokens, kD, g.page_tokens);
   if (rc) return rc;
   static bool cfg = false;
   if (!cfg) {
@@ -332,7 +370,7 @@ int launch_chunk_attention_tc(const __nv_bfloat16* qkv, int q_rows, int q_stride
   prm.layer = layer;
   prm.page_tokens = g.page_tokens;
   prm.scale_log2 = scale * 1.4426950408889634f;
-  chunk_attn_tc_kernel<<<dim3(n_work, g.n_heads), 192, kSmem, s>>>(tq, tkv, prm);
+  chunk_attn_tc_kernel<<<dim3(n_work, g.n_heads), 192, kSmem, s>>>(tq, tk, prm);
   TK_CUDA(cudaGetLastError());
   note_launch();
   if (any_split) {

@@ -929,6 +929,26 @@ int make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t
   return TK_OK;
 }
 
+// KV pool viewed as 4 KB blocks of (page, layer, head, K|V): {64 d,
+// page_tokens slots, 2 d-halves, blocks}; one box = one block, landing in
+// shared memory as [half][slot][128 B] with the 128-byte swizzle (the UMMA
+// MN-major layout of V for one page).
+int make_tmap_kv_pages(CUtensorMap* map, const void* pool, uint64_t blocks, uint32_t page_tokens) {
+  EncodeTiledFn fn = encode_fn();
+  TK_CHECK(fn != nullptr, TK_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const uint64_t row = 128 * 2;  // bytes per slot (head_dim 128)
+  cuuint64_t dims[4] = {64, page_tokens, 2, blocks};
+  cuuint64_t strides[3] = {row, 128, page_tokens * row};
+  cuuint32_t box[4] = {64, page_tokens, 2, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pool), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TK_CHECK(r == CUDA_SUCCESS, TK_ECUDA,
+           "cuTensorMapEncodeTiled (kv pages) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return TK_OK;
+}
+
 static int pick_bn(int N) { return N >= 1024 ? 256 : 128; }
 
 // Co-resident clusters of size cs for the BN variant (queried once per variant).

@@ -720,7 +720,7 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
   int n_qb = 0;
   const bool tc_attn = use_tc_attention(m.head_dim);
   const int n_work = build_attn_work(slices, n_slices, m.n_heads, qbs, qcap, work,
-                                     qcap + kAttnMaxSplitSlots, &n_qb, tc_attn ? 128 : 64);
+                                     qcap + kAttnMaxSplitSlots, &n_qb, 64);
   TK_CHECK(n_work >= 0, TK_EINVAL, "prefill: attention work list overflow");
   bool any_split = false;
   for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
@@ -1124,7 +1124,7 @@ int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_
   int n_qb = 0;
   const bool tc_attn = use_tc_attention(head_dim);
   const int n_work = build_attn_work(slices, n_slices, n_heads, qbs.data(), qcap, work.data(),
-                                     static_cast<int>(work.size()), &n_qb, tc_attn ? 128 : 64);
+                                     static_cast<int>(work.size()), &n_qb, 64);
   TK_CHECK(n_work >= 0, TK_EINVAL, "tk_chunk_attention: work list");
   bool any_split = false;
   for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;

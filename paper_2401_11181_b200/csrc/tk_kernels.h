@@ -25,7 +25,9 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
               int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas = 0);
 int64_t gemm_workspace_bytes(int M, int N, int K);
 
-// Page-major KV pool geometry: [page][layer][2][heads][page_tokens][head_dim] bf16.
+// Page-major KV pool geometry: [page][layer][head][K|V][page_tokens][head_dim] bf16.
+// K and V of one (page, layer, head) are adjacent 4 KB blocks (head_dim 128),
+// so one 5-D TMA box brings both into shared memory.
 struct KvGeom {
   int n_layers, n_heads, head_dim, page_tokens;
   __host__ __device__ size_t page_elems() const {
@@ -33,7 +35,7 @@ struct KvGeom {
   }
   // element offset of (page, layer, kv, head, slot, 0)
   __host__ __device__ size_t offset(int page, int layer, int kv, int head, int slot) const {
-    return (((static_cast<size_t>(page) * n_layers + layer) * 2 + kv) * n_heads + head) *
+    return (((static_cast<size_t>(page) * n_layers + layer) * n_heads + head) * 2 + kv) *
                static_cast<size_t>(page_tokens) * head_dim +
            static_cast<size_t>(slot) * head_dim;
   }

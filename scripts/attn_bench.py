@@ -32,10 +32,10 @@ def main():
     n_pages = (ctx + pt - 1) // pt
     g = torch.Generator(device="cuda").manual_seed(0)
     total = max(n_pages, args.pool_pages)
-    pool = torch.zeros(total, L, 2, H, pt, D, device="cuda", dtype=torch.bfloat16)
+    pool = torch.zeros(total, L, H, 2, pt, D, device="cuda", dtype=torch.bfloat16)
     perm = torch.randperm(total, generator=torch.Generator().manual_seed(1)).tolist()[:n_pages]
     for p_ in perm:
-        pool[p_] = (torch.randn(L, 2, H, pt, D, device="cuda", generator=g) * 0.5).bfloat16()
+        pool[p_] = (torch.randn(L, H, 2, pt, D, device="cuda", generator=g) * 0.5).bfloat16()
     slices = [(args.prefix, args.len, 0, n_pages, 1)]
     qkv = torch.randn(args.len, 3 * H * D, device="cuda", generator=g).bfloat16()
     layer = L - 1
@@ -50,8 +50,8 @@ def main():
     # reference on 2 heads
     err = 0.0
     for h in (0, H - 1):
-        K = torch.cat([pool[p, layer, 0, h] for p in perm], 0)[:ctx].float()
-        V = torch.cat([pool[p, layer, 1, h] for p in perm], 0)[:ctx].float()
+        K = torch.cat([pool[p, layer, h, 0] for p in perm], 0)[:ctx].float()
+        V = torch.cat([pool[p, layer, h, 1] for p in perm], 0)[:ctx].float()
         q = qkv[:, h * D:(h + 1) * D].float()
         s = (q @ K.t()) * D ** -0.5
         qpos = torch.arange(args.prefix, ctx, device="cuda")[:, None]

@@ -92,15 +92,15 @@ def test_layernorm_and_argmax():
 
 
 def _pool(n_pages, L, H, D, pt, gen):
-    return (torch.randn(n_pages, L, 2, H, pt, D, device="cuda", generator=gen) * 0.5).bfloat16()
+    return (torch.randn(n_pages, L, H, 2, pt, D, device="cuda", generator=gen) * 0.5).bfloat16()
 
 
 def _gather_kv(pool, layer, pages, n_tok, pt):
     # -> K, V [H, n_tok, D] fp32 for one request
     ks, vs = [], []
-    for p in pages:
-        ks.append(pool[p, layer, 0])
-        vs.append(pool[p, layer, 1])
+    for p in pages:  # pool: [page][layer][head][K|V][slot][d]
+        ks.append(pool[p, layer, :, 0])
+        vs.append(pool[p, layer, :, 1])
     K = torch.cat(ks, dim=1)[:, :n_tok].float()
     V = torch.cat(vs, dim=1)[:, :n_tok].float()
     return K, V

@@ -81,7 +81,9 @@ def test_prefill_and_decode_match_oracle(model):
         for rid, row_d, row_r in zip(emitting, logits, ref):
             first_dev[rid], first_ref[rid] = row_d, row_r
     # KV pages written by the device match the oracle's pages
-    got_page = bf16_bits_to_f32(inst.read_page(tables[2][3])).view(cache.pages[0].shape)
+    s_ = ora.s
+    got_page = bf16_bits_to_f32(inst.read_page(tables[2][3])).view(
+        s_.n_layers, s_.n_heads, 2, PT, s_.head_dim).transpose(1, 2)  # -> [L][K|V][H][16][D]
     assert (got_page - cache.pages[tables[2][3]]).abs().max().item() < 0.05
     # three decode steps, feeding the oracle's greedy tokens to both sides
     last = [int(first_ref[i].argmax()) for i in range(len(lens))]
