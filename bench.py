@@ -202,24 +202,30 @@ def cpu_port_sample(plan_chunks, max_seconds: float = 25.0, threads: int | None 
 
 # ---------------------------------------------------------------- arms
 
-def dist_setup():
+def dist_setup(backend: str = "nccl"):
+    """One process per GPU (torchrun env); nccl on the box, gloo in CPU tests."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
 def dist_max(value: float, world: int) -> float:
+    """Max over ranks (the timing rule: whole-job time = slowest rank)."""
     if world == 1:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -377,6 +383,8 @@ def run_ours(args, world, rank, local):
     }
     line["share_of_step"] = {k: round(v["ms"] / (dev_s * 1e3), 4) for k, v in prof.items()}
     inst.close()
+    if world == 1 and not args.no_decode:
+        line["decode"] = decode_run(args, shape, local, peaks)
     if world == 1 and not args.no_serving:
         line["serving"] = serving_run(args)
     if world == 1 and not args.no_cpu_baseline:
@@ -386,6 +394,44 @@ def run_ours(args, world, rank, local):
         line["cpu_baseline"] = {"value": round(tok_s, 3), "unit": "tok/s", "cores": cores,
                                 "kind": "port", "sample": desc}
     print(json.dumps(line))
+
+
+def decode_run(args, shape, device: int, peaks: dict) -> dict:
+    """Decode steps (tk_decode_step) at a fixed batch/context: tok/s and the
+    paged decode-attention kernel against the HBM roofline (CUDA events)."""
+    from paper_2401_11181_b200 import native
+    out = {}
+    for batch, ctx in ((32, 2048), (128, 512)):  # pools of ~55 GB each
+        steps = 16
+        pages_per = (ctx + steps + 3 + 16) // 16
+        inst = native.Instance(shape, device=device, seed=args.seed,
+                               kv_pages=batch * pages_per, max_chunk=max(64, batch))
+        bt = list(range(batch * pages_per))
+        last = [7] * batch
+        for i in range(3):
+            ev, _ = inst.decode_step(last, [ctx + i] * batch, bt, pages_per)
+            ev.wait()
+        inst.profile(True)
+        evs = [inst.decode_step(last, [ctx + 3 + i] * batch, bt, pages_per)[0]
+               for i in range(steps)]
+        ns = native.event_elapsed_ns(evs[0], evs[-1])
+        prof = inst.profile_read()
+        inst.close()
+        att = prof["attention"]
+        gbs = att["bytes"] / (att["ms"] / 1e3) / 1e9
+        gemm_ms = sum(prof[k]["ms"] for k in ("qkv_gemm", "o_gemm", "fc1_gemm", "fc2_gemm"))
+        gemm_bytes = sum(prof[k]["bytes"] for k in ("qkv_gemm", "o_gemm", "fc1_gemm", "fc2_gemm"))
+        out[f"b{batch}_ctx{ctx}"] = {
+            "decode_tok_s": round(batch * steps / (ns / 1e9), 1),
+            "step_ms": round(ns / 1e6 / steps, 3),
+            "attention_roofline": {"bound": "hbm", "achieved": round(gbs, 1),
+                                   "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                   "frac": round(gbs / peaks["hbm_gbs"], 4),
+                                   "launches": att["launches"]},
+            "gemm_weight_stream_gbs": round(gemm_bytes / (gemm_ms / 1e3) / 1e9, 1),
+            "share_of_step": {k: round(v["ms"] / (ns / 1e6), 4) for k, v in prof.items()},
+        }
+    return out
 
 
 def serving_run(args) -> dict:
@@ -432,6 +478,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-serving", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--serving-n", type=int, default=32)
     args = ap.parse_args()
     world, rank, local = dist_setup()

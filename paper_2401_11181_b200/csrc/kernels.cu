@@ -480,38 +480,51 @@ __global__ void __launch_bounds__(kAttnThreads)
   }
 }
 
-// Merge the split partials of every multi-split q-block: grid (qblocks, heads).
+// Merge the split partials of every multi-split q-block: grid (qblocks, heads),
+// 8 warps, one query row per warp at a time, lanes across the head dim (float4)
+// so every partial row is read with coalesced 16-byte accesses.
 template <int D>
-__global__ void __launch_bounds__(kAttnRows)
+__global__ void __launch_bounds__(256)
     attn_combine_kernel(__nv_bfloat16* __restrict__ o, const AttnQBlock* __restrict__ qblocks,
                         int n_heads, const float* __restrict__ partial) {
   const AttnQBlock qb = qblocks[blockIdx.x];
   if (qb.n_splits <= 1) return;
   const int head = blockIdx.y;
-  const int row = threadIdx.x;
-  if (row >= qb.nrows) return;
-  const size_t stride_slot = static_cast<size_t>(n_heads) * kAttnRows * (D + 4);
-  const float* first = partial + (static_cast<size_t>(qb.first_slot) * n_heads + head) * kAttnRows * (D + 4) +
-                       static_cast<size_t>(row) * (D + 4);
-  float M = -INFINITY;
-  for (int s = 0; s < qb.n_splits; ++s) M = fmaxf(M, first[s * stride_slot + D]);
-  float L = 0.f;
-  float wts[16];
-  for (int s = 0; s < qb.n_splits; ++s) {
-    const float m = first[s * stride_slot + D];
-    wts[s] = (m == -INFINITY) ? 0.f : exp2f(m - M);
-    L += first[s * stride_slot + D + 1] * wts[s];
-  }
-  const float inv = L > 0.f ? 1.f / L : 0.f;
-  __nv_bfloat16* out = o + static_cast<size_t>(qb.row0 + row) * n_heads * D + head * D;
-  for (int d = 0; d < D; d += 2) {
-    float a0 = 0.f, a1 = 0.f;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int RS = D + 4;  // partial row stride (floats)
+  const size_t stride_slot = static_cast<size_t>(n_heads) * kAttnRows * RS;
+  const float* base = partial + (static_cast<size_t>(qb.first_slot) * n_heads + head) * kAttnRows * RS;
+  for (int row = warp; row < qb.nrows; row += 8) {
+    const float* first = base + static_cast<size_t>(row) * RS;
+    float M = -INFINITY;
+    for (int s = 0; s < qb.n_splits; ++s) M = fmaxf(M, first[s * stride_slot + D]);
+    float L = 0.f;
+    float acc[D / 32];
+#pragma unroll
+    for (int e = 0; e < D / 32; ++e) acc[e] = 0.f;
     for (int s = 0; s < qb.n_splits; ++s) {
-      const float2 v = *reinterpret_cast<const float2*>(first + s * stride_slot + d);
-      a0 += v.x * wts[s];
-      a1 += v.y * wts[s];
+      const float* ps = first + s * stride_slot;
+      const float m = ps[D];
+      const float w = (m == -INFINITY) ? 0.f : exp2f(m - M);
+      L += ps[D + 1] * w;
+      if constexpr (D == 128) {
+        const float4 v = *reinterpret_cast<const float4*>(ps + lane * 4);
+        acc[0] += v.x * w; acc[1] += v.y * w; acc[2] += v.z * w; acc[3] += v.w * w;
+      } else {
+        const float2 v = *reinterpret_cast<const float2*>(ps + lane * 2);
+        acc[0] += v.x * w; acc[1] += v.y * w;
+      }
     }
-    *reinterpret_cast<uint32_t*>(out + d) = pack_bf16x2(a0 * inv, a1 * inv);
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    __nv_bfloat16* out = o + static_cast<size_t>(qb.row0 + row) * n_heads * D + head * D;
+    if constexpr (D == 128) {
+      uint2 pk;
+      pk.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+      pk.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+      *reinterpret_cast<uint2*>(out + lane * 4) = pk;
+    } else {
+      *reinterpret_cast<uint32_t*>(out + lane * 2) = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+    }
   }
 }
 
@@ -613,11 +626,10 @@ int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloa
 int launch_attn_combine(__nv_bfloat16* o, const AttnQBlock* qblocks, int n_qblocks, int n_heads,
                         int head_dim, float* partial, cudaStream_t s) {
   if (head_dim == 128)
-    attn_combine_kernel<128><<<dim3(n_qblocks, n_heads), kAttnRows, 0, s>>>(o, qblocks, n_heads,
-                                                                            partial);
+    attn_combine_kernel<128><<<dim3(n_qblocks, n_heads), 256, 0, s>>>(o, qblocks, n_heads,
+                                                                      partial);
   else
-    attn_combine_kernel<64><<<dim3(n_qblocks, n_heads), kAttnRows, 0, s>>>(o, qblocks, n_heads,
-                                                                           partial);
+    attn_combine_kernel<64><<<dim3(n_qblocks, n_heads), 256, 0, s>>>(o, qblocks, n_heads, partial);
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;

@@ -57,6 +57,22 @@ class _Pool:
         self.free.extend(reversed(pages))
 
 
+def place_instance(iid: str, n_prefill: int, n_dev: int, overrides: dict | None = None) -> int:
+    """CUDA ordinal of scheduler instance ``iid`` (p{i}, d{i}, c{i}).
+
+    Prefill instances take the first ordinals, decode instances the next ones
+    (2:6 on 8 GPUs -> p0,p1 on 0,1 and d0..d5 on 2..7), wrapping round-robin
+    when there are fewer devices than instances (1 GPU: co-located).  An
+    explicit ``devices`` map in the config wins.
+    """
+    if overrides and iid in overrides:
+        return int(overrides[iid]) % n_dev
+    kind, idx = iid[0], int(iid[1:])
+    if kind in ("p", "c"):
+        return idx % n_dev
+    return (n_prefill + idx) % n_dev
+
+
 class _Done:
     """A completion handle that is already complete (no device work)."""
 
@@ -120,12 +136,7 @@ class CudaExecutor:
 
     # -- lifecycle ---------------------------------------------------------------------
     def _device_of(self, iid: str) -> int:
-        if iid in self.devices:
-            return int(self.devices[iid]) % self.n_dev
-        kind, idx = iid[0], int(iid[1:])
-        if kind == "p" or kind == "c":
-            return idx % self.n_dev
-        return (self.config.n_prefill + idx) % self.n_dev
+        return place_instance(iid, self.config.n_prefill, self.n_dev, self.devices)
 
     def attach(self, inst) -> None:
         dev = self._device_of(inst.id)
