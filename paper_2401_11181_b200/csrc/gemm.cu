@@ -977,6 +977,24 @@ struct GemmPlan {
 static int max_skinny_ctas(int nb);
 static int max_pair_clusters(int cs);
 
+// Stream-K range boundaries that fall inside a tile cost a partial-tile
+// exchange.  Among cluster counts in [0.85*max, max] take the one with the
+// fewest split tiles (ties: more clusters), e.g. QKV at M=512 has 60 cluster
+// tiles -> 30 clusters own exactly two tiles each and nothing is split.
+static int pick_clusters(long long total_iters, int kbs, int max_clusters) {
+  int best = max_clusters, best_splits = 1 << 30;
+  for (int g = max_clusters; g >= std::max(1, (max_clusters * 85) / 100); --g) {
+    int splits = 0;
+    for (int c = 1; c < g; ++c)
+      if ((static_cast<long long>(c) * total_iters / g) % kbs != 0) ++splits;
+    if (splits < best_splits) {
+      best_splits = splits;
+      best = g;
+    }
+  }
+  return best;
+}
+
 static GemmPlan plan_skinny(int M, int N, int K, int max_ctas) {
   GemmPlan pl{};
   pl.skinny = true;
@@ -1017,6 +1035,7 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
   int clusters = pl.pair ? max_pair_clusters(pl.cs) : max_clusters_for(pl.bn, pl.cs);
   if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / pl.cs));
   clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, pl.total_iters / 4)));
+  if (max_ctas <= 0) clusters = pick_clusters(pl.total_iters, pl.kbs, clusters);
   pl.clusters = clusters;
   // most CTAs (clusters) sharing one tile, over all cluster tiles
   const long long ctiles = pl.total_iters / pl.kbs;
@@ -1249,6 +1268,8 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   TK_CHECK(M > 0 && N > 0 && K > 0, TK_EINVAL, "gemm: empty problem");
   TK_CHECK(K % 64 == 0, TK_EINVAL, "gemm: K must be a multiple of 64");
   TK_CHECK(N % 8 == 0, TK_EINVAL, "gemm: N must be a multiple of 8");
+  static const int env_ctas = getenv("TK_GEMM_MAX_CTAS") ? atoi(getenv("TK_GEMM_MAX_CTAS")) : 0;
+  if (max_ctas <= 0 && env_ctas > 0) max_ctas = env_ctas;  // experiments only
   const GemmPlan pl = plan_gemm(M, N, K, max_ctas);
   TK_CHECK(ws_bytes >= pl.ws_bytes, TK_EINVAL, "gemm: workspace too small");
   TK_CHECK(pl.counters_fit, TK_EINVAL, "gemm: too many tiles for the counter region");
