@@ -29,13 +29,14 @@ constexpr int kRows = 128;
 constexpr int kKeys = 64;                  // keys per KV block
 constexpr int kD = 128;
 constexpr int kStages = 4;                 // K/V blocks in flight
+constexpr int kPBuf = 2;                   // P double buffer: softmax j+1 overlaps PV j
 constexpr int kQTile = kRows * kD * 2;     // 32 KB: Q as two SW128 atom columns [128][64]
 constexpr int kQHalf = kQTile / 2;
 constexpr int kKvHalf = kKeys * 64 * 2;    // 8 KB: one d-half of a K or V block
 constexpr int kKTile = 2 * kKvHalf;        // 16 KB: [half][64 keys][128 B]
 constexpr int kStageBytes = 2 * kKTile;    // K then V
 constexpr int kPTile = kRows * kKeys * 2;  // 16 KB: P [128][64] bf16 (one atom column)
-constexpr int kSmem = kQTile + kStages * kStageBytes + 2 * kPTile + 1024 + 256;
+constexpr int kSmem = kQTile + kStages * kStageBytes + kPBuf * kPTile + 256;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
 }  // namespace
 
@@ -71,21 +72,20 @@ struct TcAttnParams {
 __global__ void __launch_bounds__(192, 1)
     chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
                          const __grid_constant__ CUtensorMap tmap_k, const TcAttnParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 atoms need 1 KB alignment
+  uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + kQTile;                           // [stage]{K [half][64][128 B], V same}
-  uint8_t* sP = sKV + kStages * kStageBytes;              // [2][128][128 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPTile);
+  uint8_t* sP = sKV + kStages * kStageBytes;              // [kPBuf][128][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBuf * kPTile);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;               // [kStages]
   uint64_t* kv_empty = kv_full + kStages;     // [kStages]
   uint64_t* s_full = kv_empty + kStages;
   uint64_t* s_free = s_full + 1;
-  uint64_t* p_full = s_free + 1;   // [2] per P buffer
-  uint64_t* o_done = p_full + 2;   // [2] per P buffer: PV_j retired (j % 2)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* p_full = s_free + 1;       // [kPBuf] per P buffer
+  uint64_t* o_done = p_full + kPBuf;   // [kPBuf]: PV_j retired (j % kPBuf)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + kPBuf);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const AttnWork w = p.work[blockIdx.x];
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(s_free, 4);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kPBuf; ++b) {
       mbar_init(&p_full[b], 4);
       mbar_init(&o_done[b], 1);
     }
@@ -171,8 +171,8 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(s_free, j & 1);  // S_j is in the softmax warps' registers
           issue_s(j + 1);
         }
-        const int pb = j & 1;
-        mbar_wait(&p_full[pb], (j >> 1) & 1);
+        const int pb = j % kPBuf;
+        mbar_wait(&p_full[pb], (j / kPBuf) & 1);
         tc_fence_after();
         const int st = j % kStages;
         const uint32_t v_addr = smem_u32(sKV + st * kStageBytes + kKTile);
@@ -211,17 +211,22 @@ __global__ void __launch_bounds__(192, 1)
       const int lim = min(qp, kv_end - 1);  // last key this row may see
       // Blocks entirely below every row's diagonal need no mask (warp-uniform).
       const bool full = __all_sync(0xffffffffu, k0 + kKeys - 1 <= lim);
-      float raw_mx = -INFINITY;
+      // 8 independent max chains (a single 64-long FMNMX chain is pure latency)
+      float mxv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) mxv[q] = -INFINITY;
       if (full) {
 #pragma unroll
-        for (int c = 0; c < kKeys; ++c) raw_mx = fmaxf(raw_mx, s[c]);
+        for (int c = 0; c < kKeys; ++c) mxv[c & 7] = fmaxf(mxv[c & 7], s[c]);
       } else {
 #pragma unroll
         for (int c = 0; c < kKeys; ++c) {
           s[c] = (k0 + c <= lim) ? s[c] : -INFINITY;
-          raw_mx = fmaxf(raw_mx, s[c]);
+          mxv[c & 7] = fmaxf(mxv[c & 7], s[c]);
         }
       }
+      const float raw_mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
+                                 fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
       const float mx = raw_mx * p.scale_log2;  // scale > 0: max commutes
       float corr = 1.f;
       bool rescale = false;
@@ -232,36 +237,38 @@ __global__ void __launch_bounds__(192, 1)
       }
       l *= corr;
       const float base = (m_used == -INFINITY) ? 0.f : m_used;
-      // P is double buffered: P_j's buffer was last read by PV_{j-2}
-      if (j > 1) {
-        mbar_wait(&o_done[j & 1], ((j >> 1) & 1) ^ 1);
+      // P_j's buffer was last read by PV_{j-kPBuf}
+      if (j >= kPBuf) {
+        mbar_wait(&o_done[j % kPBuf], ((j / kPBuf) & 1) ^ 1);
         tc_fence_after();
       }
-      uint8_t* prow = sP + (j & 1) * kPTile + r * 128;
+      uint8_t* prow = sP + (j % kPBuf) * kPTile + r * 128;
+      float lsum[8];  // 8 independent accumulation chains
 #pragma unroll
-      for (int a = 0; a < kKeys / 64; ++a) {
+      for (int q = 0; q < 8; ++q) lsum[q] = 0.f;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float e[8];
+      for (int c = 0; c < kKeys / 8; ++c) {
+        float e[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const float x = fmaf(s[a * 64 + c * 8 + t], p.scale_log2, -base);
-            e[t] = (c & 1) ? exp2_poly(x) : exp2f(x);  // FMA pipe / MUFU split
-            l += e[t];
-          }
-          uint4 pk;
-          pk.x = pack_bf16x2(e[0], e[1]);
-          pk.y = pack_bf16x2(e[2], e[3]);
-          pk.z = pack_bf16x2(e[4], e[5]);
-          pk.w = pack_bf16x2(e[6], e[7]);
-          *reinterpret_cast<uint4*>(prow + a * kPTile + ((c ^ (r & 7)) << 4)) = pk;
+        for (int t = 0; t < 8; ++t) {
+          const float x = fmaf(s[c * 8 + t], p.scale_log2, -base);
+          // 1 in 4 exponentials on the FMA pipe, the rest on MUFU (balanced issue)
+          e[t] = ((c & 3) == 3) ? exp2_poly(x) : exp2f(x);
+          lsum[t] += e[t];
         }
+        uint4 pk;
+        pk.x = pack_bf16x2(e[0], e[1]);
+        pk.y = pack_bf16x2(e[2], e[3]);
+        pk.z = pack_bf16x2(e[4], e[5]);
+        pk.w = pack_bf16x2(e[6], e[7]);
+        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = pk;
       }
+      l += ((lsum[0] + lsum[1]) + (lsum[2] + lsum[3])) + ((lsum[4] + lsum[5]) + (lsum[6] + lsum[7]));
       // tcgen05.ld/st are warp-collective: rescale if any row of the warp needs it
       // (rows that do not need it multiply by corr == 1)
       if (__any_sync(0xffffffffu, rescale && j > 0)) {
         // O must hold PV_{j-1} before it is rescaled
-        mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        mbar_wait(&o_done[(j - 1) % kPBuf], ((j - 1) / kPBuf) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < kD / 32; ++c) {
@@ -277,10 +284,10 @@ __global__ void __launch_bounds__(192, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+      if (lane == 0) mbar_arrive(&p_full[j % kPBuf]);
     }
     // final O row
-    mbar_wait(&o_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
+    mbar_wait(&o_done[(nblk - 1) % kPBuf], ((nblk - 1) / kPBuf) & 1);
     tc_fence_after();
     const int HD = p.n_heads * kD;
     if (qb.n_splits == 1) {
