@@ -446,6 +446,8 @@ def serving_run(args) -> dict:
     sim = run_experiment(tk.config_from_dict(cfg), seed=args.seed).summary
     res = run_experiment(tk.config_from_dict(dict(cfg, executor="cuda")), seed=args.seed)
     s, d = res.summary, res.summary["device"]
+    coupled_cfg = dict(cfg, system="coupled", cluster={"coupled": 1}, executor="cuda")
+    c = run_experiment(tk.config_from_dict(coupled_cfg), seed=args.seed).summary
     return {
         "workload": f"Mixed-{args.serving_n} (four-class, burst), 1 prefill + 1 decode instance "
                     f"co-located on one GPU, {args.model}, reserve_dynamic, power-of-two, "
@@ -461,6 +463,11 @@ def serving_run(args) -> dict:
         "reference_modeled": {"ttft_avg_ms": round(sim["ttft"]["avg_us"] / 1e3, 2),
                               "jct_avg_ms": round(sim["jct"]["avg_us"] / 1e3, 2),
                               "note": "pdsim cost model (V100-calibrated), same workload"},
+        "coupled_baseline": {"system": "coupled (vLLM-like, pdsim/coupled.py) on the same GPU",
+                             "ttft_avg_ms": round(c["ttft"]["avg_us"] / 1e3, 2),
+                             "jct_avg_ms": round(c["jct"]["avg_us"] / 1e3, 2),
+                             "perf_per_dollar": round(c["perf_per_dollar"], 4)},
+        "perf_per_dollar": round(s["perf_per_dollar"], 4),
     }
 
 

@@ -306,10 +306,66 @@ class CudaExecutor:
 
         return _Then(ev, publish), modeled
 
+    # -- coupled (vLLM-like) baseline: prefill and decode share one instance ------------
+    def admit_prompt(self, inst, req: Request) -> None:
+        self.tables[inst.id][req.id] = self.pools[inst.id].take(
+            costs.pages_needed(self.params, req.prompt_len), inst.id)
+        self.kv_home[req.id] = inst.id
+
     def mixed_step(self, inst, prefilling, running, prefill_tokens, kv_tokens, swapped_out,
                    swapped_in):
-        raise SimulationError("coupled instances on the CUDA executor are not supported yet "
-                              "(SURVEY.md §8(f) rank 1)")
+        """One coupled iteration (pdsim/coupled.py:82-101): the running batch decodes
+        one token, then the admitted prompts are prefilled whole (in device chunks of
+        the instance's row capacity); the iteration ends when both are done."""
+        from .prefill import chunkify
+        p = inst.params
+        modeled = costs.mixed_iter_latency(p, prefill_tokens, len(running), kv_tokens,
+                                           n_prefill=len(prefilling)) \
+            + round(p.swap_penalty_us_per_page * (swapped_out + swapped_in))
+        dev = self.insts[inst.id]
+        tables = self.tables[inst.id]
+        pending = []
+        if running:
+            stride = max(len(tables[d.req.id]) for d in running)
+            bt, last, ctx = [], [], []
+            for d in running:
+                t = tables[d.req.id]
+                bt += t + [t[0]] * (stride - len(t))
+                last.append(self.last_token.get(d.req.id, 0))
+                ctx.append(d.kv_tokens)
+            ev, out = dev.decode_step(last, ctx, bt, stride)
+            rids = [d.req.id for d in running]
+            pending.append((ev, lambda out=out, rids=rids: [
+                self.last_token.__setitem__(r, int(out[i])) for i, r in enumerate(rids)]))
+            self.stats["decode_steps"] += 1
+            self.stats["decode_tokens"] += len(rids)
+        by_id = {r.id: r for r in prefilling}
+        for chunk in chunkify(list(prefilling), dev.max_chunk):
+            ids, slices, bt, emit = [], [], [], []
+            for rid, start, n in chunk.slices:
+                req = by_id[rid]
+                ids += self._ids(req)[start:start + n]
+                e = int(start + n == req.prompt_len)
+                slices.append((start, n, len(bt), len(tables[rid]), e))
+                bt += tables[rid]
+                if e:
+                    emit.append((len(slices) - 1, rid))
+            ev, out = dev.prefill_chunk(ids, slices, bt)
+            pending.append((ev, lambda out=out, emit=emit: [
+                (self.first_token.__setitem__(r, int(out[i])),
+                 self.last_token.__setitem__(r, int(out[i]))) for i, r in emit]))
+            self.stats["prefill_tokens"] += len(ids)
+            self.stats["prefill_chunks"] += 1
+        if not pending:
+            return _Done(), modeled
+        last_ev = pending[-1][0]
+
+        def publish():
+            for ev, fn in pending:
+                ev.wait()
+                fn()
+
+        return _Then(last_ev, publish), modeled
 
     # -- reporting ---------------------------------------------------------------------------------
     def summary_extras(self) -> dict:

@@ -40,6 +40,9 @@ class SimExecutor:
     def admit(self, inst, dreq) -> None:
         pass
 
+    def admit_prompt(self, inst, req) -> None:
+        pass
+
     def grow(self, inst, dreq, pages: int) -> None:
         pass
 

@@ -26,10 +26,13 @@ def main():
     ap.add_argument("--prefill-pages", type=int, default=2048)
     ap.add_argument("--mixture", default="")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--system", default="disaggregated", choices=["disaggregated", "coupled"])
     args = ap.parse_args()
     npf, ndc = (int(x) for x in args.split.split(":"))
     cfg = {
-        "cluster": {"prefill": npf, "decode": ndc},
+        "system": args.system,
+        "cluster": {"prefill": npf, "decode": ndc} if args.system == "disaggregated"
+        else {"coupled": 1},
         "workload": {"n_requests": args.n},
         "cost_model": {"preset": "nvlink300", "mem_capacity_tokens": args.capacity},
         "model": {"name": args.model, "prefill_pages": args.prefill_pages, "staging_pages": 512,
@@ -43,7 +46,9 @@ def main():
     wall = time.perf_counter() - t0
     s, d = res.summary, res.summary["device"]
     out = {
-        "workload": f"{args.mixture or 'Mixed'}-{args.n}, {npf}P:{ndc}D, {args.model}, burst",
+        "workload": f"{args.mixture or 'Mixed'}-{args.n}, "
+                    f"{f'{npf}P:{ndc}D' if args.system == 'disaggregated' else 'coupled x1'}, "
+                    f"{args.model}, burst",
         "ttft_avg_ms": s["ttft"]["avg_us"] / 1e3, "ttft_p50_ms": s["ttft"]["p50_us"] / 1e3,
         "ttft_p99_ms": s["ttft"]["p99_us"] / 1e3,
         "jct_avg_ms": s["jct"]["avg_us"] / 1e3, "jct_p50_ms": s["jct"]["p50_us"] / 1e3,
@@ -53,6 +58,7 @@ def main():
         "decode_tok_s_device": d.get("decode_tok_s_device"),
         "decode_tok_s_wall": d["decode_tokens"] / (s["makespan_us"] / 1e6),
         "handoff_gb_s": d.get("handoff_gb_s"), "kv_bytes_sent": d["kv_bytes_sent"],
+        "resource_usage_s": s["resource_usage_us"] / 1e6, "perf_per_dollar": s["perf_per_dollar"],
         "decode_steps": d["decode_steps"], "completed": s["completed"],
         "modeled_reference": {"ttft_avg_ms": sim["ttft"]["avg_us"] / 1e3,
                               "jct_avg_ms": sim["jct"]["avg_us"] / 1e3,

@@ -65,3 +65,19 @@ def test_cuda_executor_greedy_swaps_restore_pages():
     # every physical page is back in its pool
     for iid, pool in executor.pools.items():
         assert len(pool.free) == pool.n_pages, iid
+
+
+def test_cuda_executor_coupled_baseline():
+    """The vLLM-like coupled instance (pdsim/coupled.py) on the device."""
+    cfg = dict(CFG, system="coupled", cluster={"coupled": 1}, executor="cuda")
+    executor = make_executor(tk.config_from_dict(cfg))
+    res = run_experiment(tk.config_from_dict(cfg), seed=0, executor=executor)
+    s = res.summary
+    assert s["completed"] == s["n_requests"] == 24
+    for row in res.rows:
+        assert row["ttft_us"] <= row["jct_us"]
+    reqs = tk.generate(tk.config_from_dict(cfg).workload_spec, tk.RngStreams(0).stream("workload"))
+    assert s["device"]["prefill_tokens"] == sum(r.prompt_len for r in reqs)
+    assert s["device"]["decode_tokens"] == sum(r.true_decode_len for r in reqs)
+    for pool in executor.pools.values():
+        assert len(pool.free) == pool.n_pages
