@@ -200,6 +200,14 @@ int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_
                        int32_t page_tokens, const tk_slice* slices, int32_t n_slices,
                        const int32_t* block_tables, int32_t n_tokens, float scale,
                        void* stream);
+/* Microbenchmark form of tk_chunk_attention: stages once, launches iters
+ * times back to back and reports the mean device time of launches 2..iters
+ * (CUDA events on `stream`) in *avg_us.                                      */
+int tk_chunk_attention_timed(const void* q, int32_t q_stride, void* o, const void* kv_pool,
+                             int32_t layer, int32_t n_layers, int32_t n_heads, int32_t head_dim,
+                             int32_t page_tokens, const tk_slice* slices, int32_t n_slices,
+                             const int32_t* block_tables, int32_t n_tokens, float scale,
+                             void* stream, int32_t iters, float* avg_us);
 
 #ifdef __cplusplus
 }

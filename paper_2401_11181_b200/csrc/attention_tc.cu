@@ -1,373 +1,640 @@
 // attention_tc.cu -- chunked-prefill attention (K2) on 5th-gen tensor cores.
 //
-// One CTA = one head x one <=128-row query block x one KV split (128-key
-// blocks).  Per block:  S = Q K^T  (UMMA 128x128x128 -> TMEM),  softmax by
-// warps 0-3 with one query row per thread straight out of TMEM (no shuffles),
-// P (bf16) written to shared memory in the UMMA K-major SW128 layout,
-// O += P V  (UMMA, V as an MN-major operand -> TMEM).  K and V tiles are
-// TMA-loaded from the page-major KV pool by 16 lanes of the producer warp in
-// parallel (2 KB [16 keys][64 d] boxes into [d-half][64 keys][128 B] tiles),
-// 64-key blocks in a 4-stage ring so three blocks are in flight ahead of the
-// tensor core; V is consumed as an MN-major operand.
+// Replaces the stand-in pdsim/costs.py:142-152 (chunk_cost) for the attention
+// part of one chunk: every query row of a slice attends causally over its
+// request's paged KV prefix (pdsim/prefill.py:140-165 defines the slices).
 //
-// Warp roles (192 threads): 0-3 softmax / O correction / output, 4 TMA
-// producer, 5 TMEM allocator + single-thread UMMA issuer.  The issuer runs
-// S_{j+1} as soon as the softmax warps have pulled S_j into registers, so the
-// tensor core overlaps the exponentials.  O is rescaled in TMEM only when a
-// row maximum grows by more than 2^8 (exp2 domain; decided per warp, since
-// TMEM loads/stores are warp-collective); the final normalisation uses the
-// same stale maximum, so results are exact up to fp32 rounding.
+// Work unit = one head x one *pair* of 128-row query tiles of the same slice
+// (rows r..r+255) x a range of 128-key blocks.  Both tiles share every K/V
+// block that is staged in shared memory, which halves the L2->SM traffic per
+// FLOP compared to one tile per CTA (at 128 rows per K/V tile the kernel is
+// L2-bandwidth-bound long before the tensor core is busy).
+//
+// Persistent CTAs, one per SM (320 threads):
+//   warps 0-3  softmax for tile 0, one query row per thread
+//   warps 4-7  softmax for tile 1
+//   warp  8    TMA producer: Q tiles, then K_j / V_j (2 KB [16 keys][64 d]
+//              boxes, one per page and d-half) into a 4-entry 32 KB ring
+//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+// TMEM (512 columns): S_t at 128 t, O_t at 256 + 128 t.  S_t = Q_t K_j^T
+// (UMMA 128x128x128); the softmax warps read S_t, write P_t (bf16, packed two
+// per column) back over S_t with tcgen05.st, and O_t += P_t V_j reads P_t
+// straight from TMEM (A operand in tensor memory), so P never touches shared
+// memory.  The issue order S_0(j+1) after PV_0(j), then PV_1(j), S_1(j+1)
+// ping-pongs the two tiles: while warps 0-3 exponentiate S_0, the tensor core
+// runs tile 1's MMAs and vice versa.  tcgen05.mma ops of one thread execute
+// in order, which makes "S_t(j+1) overwrites P_t(j)" safe after PV_t(j).
+//
+// Softmax: 128 scores per row per block, 3-input max (FMNMX3), packed fp32x2
+// FMA/add (FFMA2/FADD2), 3/4 of the exponentials on MUFU.EX2 and 1/4 by a
+// polynomial on the FMA pipe (MUFU throughput would otherwise equal the
+// tensor time).  O is rescaled lazily, only when a row maximum grows by more
+// than 2^8 (exp2 domain); the final normalisation uses the same stale maximum,
+// so results are exact up to fp32 rounding.
+//
+// Load balance: the (head, pair, key block) space is split stream-K style
+// into equal contiguous ranges, one per CTA; a (head, pair) cut by a range
+// boundary is computed as pieces whose unnormalised partials (O, m, l) are
+// merged by fa_combine_kernel.
 #include "tk_common.cuh"
 #include "tk_kernels.h"
 
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 namespace tk {
 
 namespace {
-constexpr int kRows = 128;
-constexpr int kKeys = 64;                  // keys per KV block
+constexpr int kRows = 128;                 // query rows per tile
+constexpr int kKeys = 128;                 // keys per KV block
 constexpr int kD = 128;
-constexpr int kStages = 4;                 // K/V blocks in flight
-constexpr int kPBuf = 2;                   // P double buffer: softmax j+1 overlaps PV j
+constexpr int kRing = 4;                   // K/V ring entries (K_j and V_j alternate)
 constexpr int kQTile = kRows * kD * 2;     // 32 KB: Q as two SW128 atom columns [128][64]
 constexpr int kQHalf = kQTile / 2;
-constexpr int kKvHalf = kKeys * 64 * 2;    // 8 KB: one d-half of a K or V block
-constexpr int kKTile = 2 * kKvHalf;        // 16 KB: [half][64 keys][128 B]
-constexpr int kStageBytes = 2 * kKTile;    // K then V
-constexpr int kPTile = kRows * kKeys * 2;  // 16 KB: P [128][64] bf16 (one atom column)
-constexpr int kSmem = kQTile + kStages * kStageBytes + kPBuf * kPTile + 256;
+constexpr int kKvHalf = kKeys * 128;       // 16 KB: one d-half of a K or V block
+constexpr int kEntry = 2 * kKvHalf;        // 32 KB
+constexpr int kBarBytes = 256;
+constexpr int kSmem = 2 * kQTile + kRing * kEntry + kBarBytes + 1024;
+constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
+constexpr int kPolyEvery = 4;             // 1 in 4 key pairs exponentiated on the FMA pipe
+constexpr int kPartStride = kD + 4;       // partial row: O[128], m, l (16-byte aligned rows)
+constexpr int kMinBlocksPerCta = 3;
 }  // namespace
 
-// 2^x on the FMA/ALU pipes (no MUFU): x = n + f with |f| <= 1/2 by the
-// magic-constant rounding trick, 2^f by a degree-5 polynomial, 2^n added to
-// the exponent field with an integer add.  -inf maps to 2^-126 ~ 0.
-__device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  // round-to-nearest split via the 1.5 * 2^23 magic constant: x = n + f, |f| <= 1/2
-  const float y = x + 12582912.f;
-  const float n = y - 12582912.f;
-  const float f = x - n;
-  float q = 1.3333558e-3f;  // 2^f, degree-5 Taylor in f*ln2 (rel. err < 3e-6 on [-1/2,1/2])
-  q = fmaf(q, f, 9.6181291e-3f);
-  q = fmaf(q, f, 5.5504109e-2f);
-  q = fmaf(q, f, 2.4022651e-1f);
-  q = fmaf(q, f, 6.9314718e-1f);
-  q = fmaf(q, f, 1.0f);
-  return __int_as_float(__float_as_int(q) + ((__float_as_int(y) - 0x4B400000) << 23));
+int64_t fa_partial_bytes() {
+  return static_cast<int64_t>(kFaMaxPieces) * 2 * kRows * kPartStride * 4;
 }
 
-struct TcAttnParams {
-  const AttnWork* work;
-  const AttnQBlock* qblocks;
+// ------------------------------------------------------------ fp32x2 helpers
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^x for a pair on the FMA pipe: x = n + f (|f| <= 1/2, magic-constant
+// rounding), 2^f by a degree-5 polynomial (rel. err < 3e-6), 2^n added to the
+// exponent field.  x is clamped at -127 so masked (-inf) scores give ~0.
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float& e1) {
+  x0 = fmaxf(x0, -127.f);
+  x1 = fmaxf(x1, -127.f);
+  const uint64_t magic = f2(12582912.f, 12582912.f);
+  const uint64_t nmagic = f2(-12582912.f, -12582912.f);
+  const uint64_t x = f2(x0, x1);
+  const uint64_t y = f2_add(x, magic);
+  const uint64_t n = f2_add(y, nmagic);
+  float n0, n1;
+  f2_split(n, n0, n1);
+  const uint64_t f = f2_add(x, f2(-n0, -n1));
+  uint64_t q = f2(1.3333558e-3f, 1.3333558e-3f);
+  q = f2_fma(q, f, f2(9.6181291e-3f, 9.6181291e-3f));
+  q = f2_fma(q, f, f2(5.5504109e-2f, 5.5504109e-2f));
+  q = f2_fma(q, f, f2(2.4022651e-1f, 2.4022651e-1f));
+  q = f2_fma(q, f, f2(6.9314718e-1f, 6.9314718e-1f));
+  q = f2_fma(q, f, f2(1.0f, 1.0f));
+  float q0, q1, y0, y1;
+  f2_split(q, q0, q1);
+  f2_split(y, y0, y1);
+  e0 = __int_as_float(__float_as_int(q0) + ((__float_as_int(y0) - 0x4B400000) << 23));
+  e1 = __int_as_float(__float_as_int(q1) + ((__float_as_int(y1) - 0x4B400000) << 23));
+}
+
+struct FaParams {
+  const FaPair* pairs;
+  const FaUnit* units;
+  const int32_t* cta_off;
   const tk_slice* slices;
   const int32_t* bt;
   __nv_bfloat16* o;
   float* partial;
-  int n_layers, n_heads, layer, page_tokens;
+  int n_layers, n_heads, layer;
   float scale_log2;
 };
 
-__global__ void __launch_bounds__(192, 1)
-    chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                         const __grid_constant__ CUtensorMap tmap_k, const TcAttnParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 atoms need 1 KB alignment
-  uint8_t* smem = smem_raw;
-  uint8_t* sQ = smem;
-  uint8_t* sKV = smem + kQTile;                           // [stage]{K [half][64][128 B], V same}
-  uint8_t* sP = sKV + kStages * kStageBytes;              // [kPBuf][128][128 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBuf * kPTile);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;               // [kStages]
-  uint64_t* kv_empty = kv_full + kStages;     // [kStages]
-  uint64_t* s_full = kv_empty + kStages;
-  uint64_t* s_free = s_full + 1;
-  uint64_t* p_full = s_free + 1;       // [kPBuf] per P buffer
-  uint64_t* o_done = p_full + kPBuf;   // [kPBuf]: PV_j retired (j % kPBuf)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + kPBuf);
+struct UnitView {
+  FaPair pr;
+  int head, kb0, nblk, piece;
+  int n[2];        // key blocks of this unit each tile computes (tile 0 may stop early)
+  int kv_end[2];   // keys [0, kv_end) exist for the tile's last row
+};
+
+__device__ __forceinline__ UnitView unit_view(const FaParams& p, int u) {
+  const FaUnit un = p.units[u];
+  UnitView v;
+  v.pr = p.pairs[un.pair];
+  v.head = un.head;
+  v.kb0 = un.kb0;
+  v.nblk = un.kb1 - un.kb0;
+  v.piece = un.piece;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int nrows = t ? v.pr.nrows1 : v.pr.nrows0;
+    v.kv_end[t] = v.pr.pos0 + t * kRows + nrows;
+    const int nb = nrows > 0 ? (v.kv_end[t] + kKeys - 1) / kKeys : 0;
+    v.n[t] = max(0, min(nb - v.kb0, v.nblk));
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    chunk_attn_fa_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                         const __grid_constant__ CUtensorMap tmap_kv, const FaParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;                       // [tile][2 d-halves][128 rows][128 B]
+  uint8_t* sKV = smem + 2 * kQTile;         // [kRing][2 d-halves][128 keys][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kRing * kEntry);
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;             // [kRing]
+  uint64_t* kv_empty = kv_full + kRing;     // [kRing]
+  uint64_t* s_full = kv_empty + kRing;      // [2] S_t in TMEM
+  uint64_t* p_full = s_full + 2;            // [2] P_t in TMEM (4 warps)
+  uint64_t* o_full = p_full + 2;            // [2] last PV_t of the unit retired
+  uint64_t* o_free = o_full + 2;            // [2] O_t read out (4 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const AttnWork w = p.work[blockIdx.x];
-  const AttnQBlock qb = p.qblocks[w.qblock];
-  const int head = blockIdx.y;
-  const tk_slice sl = p.slices[qb.slice];
-  const int32_t* pages = p.bt + sl.bt_offset;
-  const int kv_end = qb.pos0 + qb.nrows;
-  const int nblk = w.kb1 - w.kb0;
-
-  if (warp == 4 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmap_q);
-    tma_prefetch_desc(&tmap_k);
+    tma_prefetch_desc(&tmap_kv);
     mbar_init(q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < kRing; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_free, 4);
-    for (int b = 0; b < kPBuf; ++b) {
-      mbar_init(&p_full[b], 4);
-      mbar_init(&o_done[b], 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 4);
+      mbar_init(&o_full[t], 1);
+      mbar_init(&o_free[t], 4);
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc<256>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S at col 0, O at col 128
+  const uint32_t tmem = *tmem_slot;
+  const int u_begin = p.cta_off[blockIdx.x], u_end = p.cta_off[blockIdx.x + 1];
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------------------------------------ producer warp
-    // lane 0 owns the barriers; lanes 0-15 each issue one 2 KB box per block:
-    // lanes 0-7 K (page i, d-half h), lanes 8-15 V, into [half][64 keys][128 B].
-    const uint64_t pol = l2_policy_evict_first();
-    if (lane == 0) {
-      mbar_expect_tx(q_full, kQTile);
-      for (int h = 0; h < 2; ++h)
-        tma_load_2d(sQ + h * kQHalf, &tmap_q, q_full, head * kD + h * 64, qb.row0, pol);
-    }
-    const int pt = p.page_tokens;
-    for (int j = 0; j < nblk; ++j) {
-      const int st = j % kStages;
+    // lane 0 owns the barriers; lanes 0-15 each issue one 2 KB box per K or V
+    // block: page i = lane/2 of the block's 8 pages, d-half h = lane%2.
+    const uint64_t pol_q = l2_policy_evict_first();
+    const uint64_t pol_kv = l2_policy_evict_last();  // re-read by the other pairs of the head
+    int ent = 0, uc = 0;
+    for (int u = u_begin; u < u_end; ++u, ++uc) {
+      const UnitView v = unit_view(p, u);
+      const tk_slice sl = p.slices[v.pr.slice];
+      const int32_t* pages = p.bt + sl.bt_offset;
       if (lane == 0) {
-        mbar_wait(&kv_empty[st], ((j / kStages) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], kStageBytes);
+        mbar_wait(q_empty, (uc & 1) ^ 1);
+        const bool two = v.pr.nrows1 > 0;
+        mbar_expect_tx(q_full, two ? 2 * kQTile : kQTile);
+        for (int t = 0; t < (two ? 2 : 1); ++t)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sQ + t * kQTile + h * kQHalf, &tmap_q, q_full, v.head * kD + h * 64,
+                        v.pr.row0 + t * kRows, pol_q);
       }
-      __syncwarp();
-      if (lane < 16) {
-        const int kv = lane >> 3, i = (lane >> 1) & 3, h = lane & 1;
-        const int pi = (w.kb0 + j) * kKeys / pt + i;
-        const int page = pi < sl.n_pages ? pages[pi] : pages[0];  // beyond: masked
-        const int blk = ((page * p.n_layers + p.layer) * p.n_heads + head) * 2 + kv;
-        tma_load_2d(sKV + st * kStageBytes + kv * kKTile + h * kKvHalf + i * pt * 128, &tmap_k,
-                    &kv_full[st], h * 64, blk * pt, pol);
+      const int i = (lane >> 1) & 7, h = lane & 1;
+      auto page_of = [&](int kb) {
+        const int pi = kb * (kKeys / 16) + i;
+        return pi < sl.n_pages ? __ldg(pages + pi) : __ldg(pages);  // beyond: masked keys
+      };
+      int pg_next = lane < 16 ? page_of(v.kb0) : 0;
+      for (int j = 0; j < v.nblk; ++j) {
+        const int pg = pg_next;
+        if (lane < 16 && j + 1 < v.nblk) pg_next = page_of(v.kb0 + j + 1);
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv, ++ent) {
+          const int st = ent % kRing;
+          if (lane == 0) {
+            mbar_wait(&kv_empty[st], ((ent / kRing) & 1) ^ 1);
+            mbar_expect_tx(&kv_full[st], kEntry);
+          }
+          __syncwarp();
+          if (lane < 16) {
+            const int blk = ((pg * p.n_layers + p.layer) * p.n_heads + v.head) * 2 + kv;
+            tma_load_2d(sKV + st * kEntry + h * kKvHalf + i * 16 * 128, &tmap_kv, &kv_full[st],
+                        h * 64, blk * 16, pol_kv);
+          }
+        }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       // ------------------------------------------------------------ UMMA issuer
       constexpr uint32_t idesc_s = umma_idesc_bf16(kRows, kKeys);
       constexpr uint32_t idesc_pv = umma_idesc_bf16(kRows, kD) | (1u << 16);  // B MN-major
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      const uint32_t q_addr = smem_u32(sQ);
-      auto issue_s = [&](int j) {
-        const int st = j % kStages;
-        mbar_wait(&kv_full[st], (j / kStages) & 1);
+      int ent = 0, uc = 0;
+      uint32_t pc[2] = {0, 0}, oc[2] = {0, 0};
+      for (int u = u_begin; u < u_end; ++u, ++uc) {
+        const UnitView v = unit_view(p, u);
+        mbar_wait(q_full, uc & 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(sKV + st * kStageBytes);
+        auto entry_addr = [&](int e) {
+          const int st = e % kRing;
+          mbar_wait(&kv_full[st], (e / kRing) & 1);
+          tc_fence_after();
+          return smem_u32(sKV + st * kEntry);
+        };
+        auto issue_s = [&](int t, uint32_t k_addr) {
+          const uint32_t q_addr = smem_u32(sQ + t * kQTile);
 #pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk)
-          umma_bf16(tmem, umma_desc_sw128(q_addr + (kk >> 2) * kQHalf + (kk & 3) * 32),
-                    umma_desc_sw128(k_addr + (kk >> 2) * kKvHalf + (kk & 3) * 32), idesc_s,
-                    kk > 0 ? 1u : 0u);
-        umma_commit(s_full);
-      };
-      issue_s(0);
-      for (int j = 0; j < nblk; ++j) {
-        if (j + 1 < nblk) {
-          mbar_wait(s_free, j & 1);  // S_j is in the softmax warps' registers
-          issue_s(j + 1);
+          for (int kk = 0; kk < kD / 16; ++kk)
+            umma_bf16(tmem + t * 128,
+                      umma_desc_sw128(q_addr + (kk >> 2) * kQHalf + (kk & 3) * 32),
+                      umma_desc_sw128(k_addr + (kk >> 2) * kKvHalf + (kk & 3) * 32), idesc_s,
+                      kk > 0 ? 1u : 0u);
+          umma_commit(&s_full[t]);
+        };
+        // block 0: S_0(0), S_1(0)
+        {
+          const uint32_t k_addr = entry_addr(ent);
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            if (v.n[t] > 0) issue_s(t, k_addr);
+          umma_commit(&kv_empty[ent % kRing]);
+          if (v.nblk == 1) umma_commit(q_empty);
         }
-        const int pb = j % kPBuf;
-        mbar_wait(&p_full[pb], (j / kPBuf) & 1);
-        tc_fence_after();
-        const int st = j % kStages;
-        const uint32_t v_addr = smem_u32(sKV + st * kStageBytes + kKTile);
-        const uint32_t p_addr = smem_u32(sP + pb * kPTile);
+        for (int j = 0; j < v.nblk; ++j) {
+          const int ek = ent + 2 * j, ev = ek + 1, ek_next = ek + 2;
+          uint32_t v_addr = 0, k_next = 0;
+          bool have_v = false, have_k = false;
 #pragma unroll
-        for (int kk = 0; kk < kKeys / 16; ++kk)  // V: MN-major, d-halves 8 KB apart
-          umma_bf16(tmem + kKeys, umma_desc_sw128(p_addr + kk * 32),
-                    umma_desc_sw128_mn(v_addr + kk * 2048, kKvHalf, 1024), idesc_pv,
-                    (j > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&o_done[pb]);
-        umma_commit(&kv_empty[st]);
+          for (int t = 0; t < 2; ++t) {
+            if (j >= v.n[t]) continue;
+            mbar_wait(&p_full[t], pc[t] & 1);
+            ++pc[t];
+            tc_fence_after();
+            if (j == 0) {
+              mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
+              ++oc[t];
+              tc_fence_after();
+            }
+            if (!have_v) {
+              v_addr = entry_addr(ev);
+              have_v = true;
+            }
+#pragma unroll
+            for (int kk = 0; kk < kKeys / 16; ++kk)  // V: MN-major, d-halves 16 KB apart
+              umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                           umma_desc_sw128_mn(v_addr + kk * 2048, kKvHalf, 1024), idesc_pv,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+            if (j == v.n[t] - 1) umma_commit(&o_full[t]);
+            if (j + 1 < v.n[t]) {
+              if (!have_k) {
+                k_next = entry_addr(ek_next);
+                have_k = true;
+              }
+              issue_s(t, k_next);
+            }
+          }
+          umma_commit(&kv_empty[ev % kRing]);
+          if (j + 1 < v.nblk) umma_commit(&kv_empty[ek_next % kRing]);
+          if (j + 2 == v.nblk) umma_commit(q_empty);  // the unit's last S has been issued
+        }
+        ent += 2 * v.nblk;
       }
     }
   } else {
     // -------------------------------------------------------------- softmax warps
-    const int r = static_cast<int>(warp * 32 + lane);
-    const int qp = qb.pos0 + r;
-    const uint32_t t_lane = tmem + ((warp * 32) << 16);
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < nblk; ++j) {
-      mbar_wait(s_full, j & 1);
-      tc_fence_after();
-      float s[kKeys];
-#pragma unroll
-      for (int c = 0; c < kKeys / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld_32x32b_x32(t_lane + c * 32, u);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(u[e]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_free);
-      const int k0 = (w.kb0 + j) * kKeys;
-      const int lim = min(qp, kv_end - 1);  // last key this row may see
-      // Blocks entirely below every row's diagonal need no mask (warp-uniform).
-      const bool full = __all_sync(0xffffffffu, k0 + kKeys - 1 <= lim);
-      // 8 independent max chains (a single 64-long FMNMX chain is pure latency)
-      float mxv[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) mxv[q] = -INFINITY;
-      if (full) {
-#pragma unroll
-        for (int c = 0; c < kKeys; ++c) mxv[c & 7] = fmaxf(mxv[c & 7], s[c]);
-      } else {
-#pragma unroll
-        for (int c = 0; c < kKeys; ++c) {
-          s[c] = (k0 + c <= lim) ? s[c] : -INFINITY;
-          mxv[c & 7] = fmaxf(mxv[c & 7], s[c]);
+    const int t = static_cast<int>(warp >> 2);
+    const int r = static_cast<int>((warp & 3) * 32 + lane);
+    const uint32_t t_lane = tmem + (((warp & 3) * 32) << 16);
+    const uint32_t t_s = t_lane + t * 128;
+    const uint32_t t_o = t_lane + 256 + t * 128;
+    const int HD = p.n_heads * kD;
+    const float sc = p.scale_log2;
+    uint32_t s_cnt = 0, o_cnt = 0;
+    for (int u = u_begin; u < u_end; ++u) {
+      const UnitView v = unit_view(p, u);
+      const int nrows = t ? v.pr.nrows1 : v.pr.nrows0;
+      const int n_t = t ? v.n[1] : v.n[0];
+      const int kv_end_t = t ? v.kv_end[1] : v.kv_end[0];
+      if (n_t == 0) {
+        if (v.piece >= 0 && nrows > 0) {  // nothing visible in this piece: empty partial
+          float* dst = p.partial + ((static_cast<size_t>(v.piece) * 2 + t) * kRows + r) * kPartStride;
+          for (int c = 0; c < kD; c += 4)
+            *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          dst[kD] = -INFINITY;
+          dst[kD + 1] = 0.f;
         }
+        continue;
       }
-      const float raw_mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
-                                 fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
-      const float mx = raw_mx * p.scale_log2;  // scale > 0: max commutes
-      float corr = 1.f;
-      bool rescale = false;
-      if (mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx != -INFINITY)) {
-        corr = (m_used == -INFINITY) ? 0.f : exp2f(m_used - mx);
-        m_used = mx;
-        rescale = true;
-      }
-      l *= corr;
-      const float base = (m_used == -INFINITY) ? 0.f : m_used;
-      // P_j's buffer was last read by PV_{j-kPBuf}
-      if (j >= kPBuf) {
-        mbar_wait(&o_done[j % kPBuf], ((j / kPBuf) & 1) ^ 1);
+      const int qp = v.pr.pos0 + t * kRows + r;
+      const int lim = min(qp, kv_end_t - 1);  // last key this row may see
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_t; ++j) {
+        mbar_wait(&s_full[t], s_cnt & 1);
+        ++s_cnt;
         tc_fence_after();
-      }
-      uint8_t* prow = sP + (j % kPBuf) * kPTile + r * 128;
-      float lsum[8];  // 8 independent accumulation chains
+        float s[kKeys];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) lsum[q] = 0.f;
-#pragma unroll
-      for (int c = 0; c < kKeys / 8; ++c) {
-        float e[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const float x = fmaf(s[c * 8 + t], p.scale_log2, -base);
-          // 1 in 4 exponentials on the FMA pipe, the rest on MUFU (balanced issue)
-          e[t] = ((c & 3) == 3) ? exp2_poly(x) : exp2f(x);
-          lsum[t] += e[t];
-        }
-        uint4 pk;
-        pk.x = pack_bf16x2(e[0], e[1]);
-        pk.y = pack_bf16x2(e[2], e[3]);
-        pk.z = pack_bf16x2(e[4], e[5]);
-        pk.w = pack_bf16x2(e[6], e[7]);
-        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = pk;
-      }
-      l += ((lsum[0] + lsum[1]) + (lsum[2] + lsum[3])) + ((lsum[4] + lsum[5]) + (lsum[6] + lsum[7]));
-      // tcgen05.ld/st are warp-collective: rescale if any row of the warp needs it
-      // (rows that do not need it multiply by corr == 1)
-      if (__any_sync(0xffffffffu, rescale && j > 0)) {
-        // O must hold PV_{j-1} before it is rescaled
-        mbar_wait(&o_done[(j - 1) % kPBuf], ((j - 1) / kPBuf) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < kD / 32; ++c) {
-          uint32_t u[32];
-          tmem_ld_32x32b_x32(t_lane + kKeys + c * 32, u);
+        for (int c = 0; c < kKeys / 32; ++c) {
+          uint32_t w[32];
+          tmem_ld_32x32b_x32(t_s + c * 32, w);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * corr);
-          tmem_st_32x32b_x32(t_lane + kKeys + c * 32, u);
+          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(w[e]);
         }
-        tmem_wait_st();
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j % kPBuf]);
-    }
-    // final O row
-    mbar_wait(&o_done[(nblk - 1) % kPBuf], ((nblk - 1) / kPBuf) & 1);
-    tc_fence_after();
-    const int HD = p.n_heads * kD;
-    if (qb.n_splits == 1) {
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* out = p.o + static_cast<size_t>(qb.row0 + r) * HD + head * kD;
-#pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld_32x32b_x32(t_lane + kKeys + c * 32, u);
-        tmem_wait_ld();
-        if (r < qb.nrows) {
+        const int k0 = (v.kb0 + j) * kKeys;
+        // blocks entirely below every row's diagonal need no mask (warp-uniform)
+        if (!__all_sync(0xffffffffu, k0 + kKeys - 1 <= lim)) {
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            uint4 pk;
-            pk.x = pack_bf16x2(__uint_as_float(u[g * 8 + 0]) * inv, __uint_as_float(u[g * 8 + 1]) * inv);
-            pk.y = pack_bf16x2(__uint_as_float(u[g * 8 + 2]) * inv, __uint_as_float(u[g * 8 + 3]) * inv);
-            pk.z = pack_bf16x2(__uint_as_float(u[g * 8 + 4]) * inv, __uint_as_float(u[g * 8 + 5]) * inv);
-            pk.w = pack_bf16x2(__uint_as_float(u[g * 8 + 6]) * inv, __uint_as_float(u[g * 8 + 7]) * inv);
-            *reinterpret_cast<uint4*>(out + c * 32 + g * 8) = pk;
+          for (int c = 0; c < kKeys; ++c) s[c] = (k0 + c <= lim) ? s[c] : -INFINITY;
+        }
+        float mx4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx4[q] = fmax3(s[2 * q], s[2 * q + 1], -INFINITY);
+#pragma unroll
+        for (int c = 8; c < kKeys; c += 8) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) mx4[q] = fmax3(mx4[q], s[c + 2 * q], s[c + 2 * q + 1]);
+        }
+        const float raw_mx = fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]);
+        const float mx = raw_mx * sc;  // scale > 0: max commutes
+        float corr = 1.f;
+        bool rescale = false;
+        if (mx > m_used + kRescaleThreshold || (m_used == -INFINITY && mx != -INFINITY)) {
+          corr = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
+          m_used = mx;
+          rescale = true;
+        }
+        l *= corr;
+        // tcgen05.ld/st are warp-collective: rescale if any row of the warp needs it.
+        // S_t(j) retired => PV_t(j-1) retired (in-order), so O_t is final here.
+        if (__any_sync(0xffffffffu, rescale && j > 0)) {
+#pragma unroll 1
+          for (int c = 0; c < kD / 32; ++c) {
+            uint32_t w[32];
+            tmem_ld_32x32b_x32(t_o + c * 32, w);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) w[e] = __float_as_uint(__uint_as_float(w[e]) * corr);
+            tmem_st_32x32b_x32(t_o + c * 32, w);
           }
         }
-      }
-    } else {
-      float* dst = p.partial +
-                   ((static_cast<size_t>(w.slot) * p.n_heads + head) * kRows + r) * (kD + 4);  // 16-byte aligned rows
-#pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld_32x32b_x32(t_lane + kKeys + c * 32, u);
-        tmem_wait_ld();
+        const float base = (m_used == -INFINITY) ? 0.f : m_used;
+        const uint64_t sc2 = f2(sc, sc), nb2 = f2(-base, -base);
+        uint64_t sum2[2] = {f2(0.f, 0.f), f2(0.f, 0.f)};
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-          *reinterpret_cast<float4*>(dst + c * 32 + g * 4) =
-              make_float4(__uint_as_float(u[g * 4]), __uint_as_float(u[g * 4 + 1]),
-                          __uint_as_float(u[g * 4 + 2]), __uint_as_float(u[g * 4 + 3]));
+        for (int c = 0; c < kKeys / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int k = c * 32 + 2 * i;
+            float x0, x1, e0, e1;
+            f2_split(f2_fma(f2(s[k], s[k + 1]), sc2, nb2), x0, x1);
+            if ((i % kPolyEvery) == kPolyEvery - 1) {
+              exp2_poly2(x0, x1, e0, e1);
+            } else {
+              e0 = ex2(x0);
+              e1 = ex2(x1);
+            }
+            sum2[i & 1] = f2_add(sum2[i & 1], f2(e0, e1));
+            pk[i] = pack_bf16x2(e0, e1);
+          }
+          tmem_st_32x32b_x16(t_s + c * 16, pk);
+        }
+        float a0, a1, b0, b1;
+        f2_split(sum2[0], a0, a1);
+        f2_split(sum2[1], b0, b1);
+        l += (a0 + a1) + (b0 + b1);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
       }
-      dst[kD] = m_used;
-      dst[kD + 1] = l;
+      // ---- epilogue: O_t -> bf16 rows (or an unnormalised partial)
+      mbar_wait(&o_full[t], o_cnt & 1);
+      ++o_cnt;
+      tc_fence_after();
+      if (v.piece < 0) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* out =
+            p.o + static_cast<size_t>(v.pr.row0 + t * kRows + r) * HD + v.head * kD;
+#pragma unroll 1
+        for (int c = 0; c < kD / 32; ++c) {
+          uint32_t w[32];
+          tmem_ld_32x32b_x32(t_o + c * 32, w);
+          tmem_wait_ld();
+          if (r < nrows) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              uint4 pk;
+              pk.x = pack_bf16x2(__uint_as_float(w[g * 8 + 0]) * inv, __uint_as_float(w[g * 8 + 1]) * inv);
+              pk.y = pack_bf16x2(__uint_as_float(w[g * 8 + 2]) * inv, __uint_as_float(w[g * 8 + 3]) * inv);
+              pk.z = pack_bf16x2(__uint_as_float(w[g * 8 + 4]) * inv, __uint_as_float(w[g * 8 + 5]) * inv);
+              pk.w = pack_bf16x2(__uint_as_float(w[g * 8 + 6]) * inv, __uint_as_float(w[g * 8 + 7]) * inv);
+              *reinterpret_cast<uint4*>(out + c * 32 + g * 8) = pk;
+            }
+          }
+        }
+      } else {
+        float* dst = p.partial + ((static_cast<size_t>(v.piece) * 2 + t) * kRows + r) * kPartStride;
+#pragma unroll 1
+        for (int c = 0; c < kD / 32; ++c) {
+          uint32_t w[32];
+          tmem_ld_32x32b_x32(t_o + c * 32, w);
+          tmem_wait_ld();
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            *reinterpret_cast<float4*>(dst + c * 32 + g * 4) =
+                make_float4(__uint_as_float(w[g * 4]), __uint_as_float(w[g * 4 + 1]),
+                            __uint_as_float(w[g * 4 + 2]), __uint_as_float(w[g * 4 + 3]));
+        }
+        dst[kD] = m_used;
+        dst[kD + 1] = l;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[t]);
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc<256>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+// Merge the pieces of every split (pair, head): one warp per query row, each
+// lane 4 of the 128 dims; partials are read coalesced (512 B per piece-row).
+__global__ void __launch_bounds__(256)
+    fa_combine_kernel(__nv_bfloat16* __restrict__ o, const FaPair* __restrict__ pairs,
+                      const FaGroup* __restrict__ groups, int n_heads,
+                      const float* __restrict__ partial) {
+  const int pair = blockIdx.x >> 5, t = (blockIdx.x >> 4) & 1, rg = blockIdx.x & 15;
+  const int head = blockIdx.y;
+  const FaGroup g = groups[pair * n_heads + head];
+  if (g.n_pieces <= 1) return;
+  const FaPair pr = pairs[pair];
+  const int nrows = t ? pr.nrows1 : pr.nrows0;
+  const int r = rg * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= nrows) return;
+  auto row_of = [&](int x) {
+    return partial + ((static_cast<size_t>(g.first_piece + x) * 2 + t) * kRows + r) * kPartStride;
+  };
+  float M = -INFINITY;
+  for (int x = 0; x < g.n_pieces; ++x) M = fmaxf(M, __ldcg(row_of(x) + kD));
+  float L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int x = 0; x < g.n_pieces; ++x) {
+    const float* src = row_of(x);
+    const float m = __ldcg(src + kD);
+    const float w = (m == -INFINITY) ? 0.f : exp2f(m - M);
+    L += w * __ldcg(src + kD + 1);
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(src) + lane);
+    acc.x += w * v.x;
+    acc.y += w * v.y;
+    acc.z += w * v.z;
+    acc.w += w * v.w;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  uint2 pk;
+  pk.x = pack_bf16x2(acc.x * inv, acc.y * inv);
+  pk.y = pack_bf16x2(acc.z * inv, acc.w * inv);
+  *reinterpret_cast<uint2*>(o + static_cast<size_t>(pr.row0 + t * kRows + r) * n_heads * kD +
+                            head * kD + lane * 4) = pk;
+}
+
+// ------------------------------------------------------------------ host side
+__host__ __forceinline__ static int owner_cta(long long b, long long T, int G) {
+  return static_cast<int>(((b + 1) * G + T - 1) / T) - 1;
+}
+
+int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_ctas, FaPlan* plan,
+                  FaPair* pairs, int pcap, FaUnit* units, int ucap, FaGroup* groups, int gcap,
+                  int32_t* cta_off, int ocap) {
+  int np = 0, row = 0;
+  long long per_head = 0;
+  for (int i = 0; i < n_slices; ++i) {
+    const tk_slice& sl = slices[i];
+    for (int r = 0; r < sl.len; r += 2 * kRows) {
+      if (np >= pcap) return -1;
+      FaPair& pr = pairs[np++];
+      pr.slice = i;
+      pr.row0 = row + r;
+      pr.pos0 = sl.start + r;
+      pr.nrows0 = std::min(kRows, sl.len - r);
+      pr.nrows1 = std::max(0, std::min(kRows, sl.len - r - kRows));
+      const int kv_end = pr.pos0 + (pr.nrows1 > 0 ? kRows + pr.nrows1 : pr.nrows0);
+      pr.nblk = (kv_end + kKeys - 1) / kKeys;
+      per_head += pr.nblk;
+    }
+    row += sl.len;
+  }
+  if (np * n_heads > gcap) return -1;
+  const long long T = per_head * n_heads;
+  int G = static_cast<int>(std::min<long long>(std::max(1, max_ctas),
+                                               std::max<long long>(1, T / kMinBlocksPerCta)));
+  if (G + 1 > ocap) return -1;
+  int nu = 0, piece = 0;
+  long long cur = 0;
+  for (int h = 0; h < n_heads; ++h) {
+    for (int q = 0; q < np; ++q) {
+      const int nb = pairs[q].nblk;
+      const int first = nu;
+      int s = 0;
+      while (s < nb) {
+        const int c = owner_cta(cur, T, G);
+        const long long end_c = static_cast<long long>(c + 1) * T / G;
+        const int take = static_cast<int>(std::min<long long>(nb - s, end_c - cur));
+        if (nu >= ucap) return -1;
+        units[nu++] = FaUnit{q, h, s, s + take, -1};
+        s += take;
+        cur += take;
+      }
+      FaGroup& g = groups[q * n_heads + h];
+      g.n_pieces = nu - first;
+      g.first_piece = -1;
+      if (g.n_pieces > 1) {
+        if (piece + g.n_pieces > kFaMaxPieces) return -1;
+        g.first_piece = piece;
+        for (int k = first; k < nu; ++k) units[k].piece = piece++;
+      }
+    }
+  }
+  // CTA c owns the units whose first block lies in its range
+  std::vector<long long> start(nu);
+  {
+    long long b = 0;
+    for (int k = 0; k < nu; ++k) {
+      start[k] = b;
+      b += units[k].kb1 - units[k].kb0;
+    }
+  }
+  int k = 0;
+  for (int c = 0; c <= G; ++c) {
+    while (k < nu && owner_cta(start[k], T, G) < c) ++k;
+    cta_off[c] = k;
+  }
+  cta_off[G] = nu;
+  plan->n_pairs = np;
+  plan->n_units = nu;
+  plan->n_ctas = G;
+  plan->n_pieces = piece;
+  return 0;
 }
 
 int make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                      uint32_t box_rows);
-int make_tmap_kv_pages(CUtensorMap* map, const void* pool, uint64_t blocks, uint32_t page_tokens);
 
-// Q rows live in the fused qkv buffer: a [rows, row_elems] map, 128 x 64 boxes.
-static int make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint64_t row_elems,
-                          uint32_t box_rows) {
-  return make_tmap_kmajor(map, base, rows, row_elems, box_rows);
-}
-
-int launch_chunk_attention_tc(const __nv_bfloat16* qkv, int q_rows, int q_stride,
+int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride,
                               __nv_bfloat16* o, const __nv_bfloat16* pool, int pool_pages,
-                              KvGeom g, int layer, const AttnWork* work, int n_work,
-                              const AttnQBlock* qblocks, int n_qblocks, bool any_split,
-                              const tk_slice* slices_dev, const int32_t* bt_dev, float scale,
-                              float* partial, cudaStream_t s) {
+                              KvGeom g, int layer, const FaPlan& plan, const FaPair* pairs_dev,
+                              const FaUnit* units_dev, const FaGroup* groups_dev,
+                              const int32_t* cta_off_dev, const tk_slice* slices_dev,
+                              const int32_t* bt_dev, float scale, float* partial,
+                              cudaStream_t s) {
   TK_CHECK(g.head_dim == kD, TK_EUNSUPPORTED, "tcgen05 attention: head_dim 128");
   TK_CHECK(g.page_tokens == 16, TK_EUNSUPPORTED, "tcgen05 attention: 16-token pages");
-  if (n_work == 0) return TK_OK;
-  CUtensorMap tq, tk;
-  int rc = make_tmap_rows(&tq, qkv, q_rows, q_stride, kRows);
+  if (plan.n_units == 0) return TK_OK;
+  CUtensorMap tq, tkv;
+  int rc = make_tmap_kmajor(&tq, qkv, q_rows, q_stride, kRows);
   if (rc) return rc;
   const uint64_t blocks = static_cast<uint64_t>(pool_pages) * g.n_layers * g.n_heads * 2;
-  rc = make_tmap_rows(&tk, pool, blocks * g.page_tokens, kD, g.page_tokens);
+  rc = make_tmap_kmajor(&tkv, pool, blocks * g.page_tokens, kD, g.page_tokens);
   if (rc) return rc;
   static bool cfg = false;
   if (!cfg) {
-    TK_CUDA(cudaFuncSetAttribute(chunk_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmem));
+    TK_CUDA(cudaFuncSetAttribute(chunk_attn_fa_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     cfg = true;
   }
-  TcAttnParams prm;
-  prm.work = work;
-  prm.qblocks = qblocks;
+  FaParams prm;
+  prm.pairs = pairs_dev;
+  prm.units = units_dev;
+  prm.cta_off = cta_off_dev;
   prm.slices = slices_dev;
   prm.bt = bt_dev;
   prm.o = o;
@@ -375,14 +642,15 @@ int launch_chunk_attention_tc(const __nv_bfloat16* qkv, int q_rows, int q_stride
   prm.n_layers = g.n_layers;
   prm.n_heads = g.n_heads;
   prm.layer = layer;
-  prm.page_tokens = g.page_tokens;
   prm.scale_log2 = scale * 1.4426950408889634f;
-  chunk_attn_tc_kernel<<<dim3(n_work, g.n_heads), 192, kSmem, s>>>(tq, tk, prm);
+  chunk_attn_fa_kernel<<<plan.n_ctas, kThreads, kSmem, s>>>(tq, tkv, prm);
   TK_CUDA(cudaGetLastError());
   note_launch();
-  if (any_split) {
-    rc = launch_attn_combine(o, qblocks, n_qblocks, g.n_heads, g.head_dim, partial, s);
-    if (rc) return rc;
+  if (plan.n_pieces > 0) {
+    fa_combine_kernel<<<dim3(plan.n_pairs * 32, g.n_heads), 256, 0, s>>>(o, pairs_dev, groups_dev,
+                                                                       g.n_heads, partial);
+    TK_CUDA(cudaGetLastError());
+    note_launch();
   }
   return TK_OK;
 }

@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(256)
 }
 
 int64_t attn_partial_bytes(int n_heads, int head_dim) {
+  if (use_tc_attention(head_dim)) return fa_partial_bytes();
   return static_cast<int64_t>(kAttnMaxSplitSlots) * n_heads * kAttnRows * (head_dim + 4) * 4;
 }
 

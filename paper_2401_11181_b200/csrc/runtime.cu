@@ -712,18 +712,37 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
   const int n_emit = static_cast<int>(emit_rows.size());
   int32_t* emit_d;
   pk.put(emit_rows.data(), n_emit, &emit_d);
-  const int qcap = n_slices + n_tokens / 128 + 1;
-  AttnQBlock* qb_d;
-  AttnQBlock* qbs = pk.put<AttnQBlock>(nullptr, qcap, &qb_d);
-  AttnWork* work_d;
-  AttnWork* work = pk.put<AttnWork>(nullptr, qcap + kAttnMaxSplitSlots, &work_d);
-  int n_qb = 0;
   const bool tc_attn = use_tc_attention(m.head_dim);
-  const int n_work = build_attn_work(slices, n_slices, m.n_heads, qbs, qcap, work,
-                                     qcap + kAttnMaxSplitSlots, &n_qb, 64);
-  TK_CHECK(n_work >= 0, TK_EINVAL, "prefill: attention work list overflow");
+  AttnQBlock* qb_d = nullptr;
+  AttnWork* work_d = nullptr;
+  int n_qb = 0, n_work = 0;
   bool any_split = false;
-  for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
+  FaPlan fa{};
+  FaPair* fa_pairs_d = nullptr;
+  FaUnit* fa_units_d = nullptr;
+  FaGroup* fa_groups_d = nullptr;
+  int32_t* fa_off_d = nullptr;
+  if (tc_attn) {
+    const int pcap = n_slices + n_tokens / 256 + 1;
+    const int ucap = pcap * m.n_heads + kNumSMs + 1;
+    FaPair* pairs = pk.put<FaPair>(nullptr, pcap, &fa_pairs_d);
+    FaUnit* units = pk.put<FaUnit>(nullptr, ucap, &fa_units_d);
+    FaGroup* groups = pk.put<FaGroup>(nullptr, pcap * m.n_heads, &fa_groups_d);
+    int32_t* off = pk.put<int32_t>(nullptr, kNumSMs + 1, &fa_off_d);
+    TK_CHECK(pk.ok(), TK_EINVAL, "prefill: metadata exceeds staging slot");
+    TK_CHECK(build_fa_plan(slices, n_slices, m.n_heads, kNumSMs, &fa, pairs, pcap, units, ucap,
+                           groups, pcap * m.n_heads, off, kNumSMs + 1) == 0,
+             TK_EINVAL, "prefill: attention plan overflow");
+  } else {
+    const int qcap = n_slices + n_tokens / 128 + 1;
+    AttnQBlock* qbs = pk.put<AttnQBlock>(nullptr, qcap, &qb_d);
+    AttnWork* work = pk.put<AttnWork>(nullptr, qcap + kAttnMaxSplitSlots, &work_d);
+    TK_CHECK(pk.ok(), TK_EINVAL, "prefill: metadata exceeds staging slot");
+    n_work = build_attn_work(slices, n_slices, m.n_heads, qbs, qcap, work,
+                             qcap + kAttnMaxSplitSlots, &n_qb, 64);
+    TK_CHECK(n_work >= 0, TK_EINVAL, "prefill: attention work list overflow");
+    for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
+  }
   int32_t* out_d;
   int32_t* out_h = pk.put<int32_t>(nullptr, std::max(1, n_slices), &out_d);
   int32_t* tok_d;
@@ -751,9 +770,10 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
   for (int l = 0; l < m.n_layers; ++l) {
     rc = run_layer(inst, l, n_tokens, meta_d, s, attn_flops, attn_bytes, [&]() {
       if (tc_attn)
-        return launch_chunk_attention_tc(inst->qkv, inst->max_chunk, 3 * h, inst->attn, inst->pool,
-                                         inst->kv_pages, inst->geom, l, work_d, n_work, qb_d, n_qb,
-                                         any_split, sl_d, bt_d, scale, inst->attn_partial, s);
+        return launch_chunk_attention_fa(inst->qkv, inst->max_chunk, 3 * h, inst->attn, inst->pool,
+                                         inst->kv_pages, inst->geom, l, fa, fa_pairs_d, fa_units_d,
+                                         fa_groups_d, fa_off_d, sl_d, bt_d, scale,
+                                         inst->attn_partial, s);
       return launch_chunk_attention_work(inst->qkv, 3 * h, inst->attn, inst->pool, inst->geom, l,
                                          work_d, n_work, qb_d, n_qb, any_split, sl_d, bt_d, scale,
                                          inst->attn_partial, s);
@@ -1111,44 +1131,83 @@ int tk_paged_decode_attention(const void* q, void* o, const void* kv_pool, int32
                                  workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
-int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_pool,
-                       int32_t layer, int32_t n_layers, int32_t n_heads, int32_t head_dim,
-                       int32_t page_tokens, const tk_slice* slices, int32_t n_slices,
-                       const int32_t* block_tables, int32_t n_tokens, float scale, void* stream) {
+static int chunk_attention_impl(const void* q, int32_t q_stride, void* o, const void* kv_pool,
+                                int32_t layer, int32_t n_layers, int32_t n_heads,
+                                int32_t head_dim, int32_t page_tokens, const tk_slice* slices,
+                                int32_t n_slices, const int32_t* block_tables, int32_t n_tokens,
+                                float scale, void* stream, int32_t iters, float* avg_us) {
   TK_CHECK(slices && block_tables && n_slices > 0, TK_EINVAL, "tk_chunk_attention: arguments");
   int n_bt = 0;
   for (int i = 0; i < n_slices; ++i) n_bt = std::max(n_bt, slices[i].bt_offset + slices[i].n_pages);
-  const int qcap = n_slices + n_tokens / 128 + 1;
-  std::vector<AttnQBlock> qbs(qcap);
-  std::vector<AttnWork> work(qcap + kAttnMaxSplitSlots);
-  int n_qb = 0;
   const bool tc_attn = use_tc_attention(head_dim);
-  const int n_work = build_attn_work(slices, n_slices, n_heads, qbs.data(), qcap, work.data(),
-                                     static_cast<int>(work.size()), &n_qb, 64);
-  TK_CHECK(n_work >= 0, TK_EINVAL, "tk_chunk_attention: work list");
-  bool any_split = false;
-  for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  void *d_sl, *d_bt, *d_work, *d_qb, *d_part;
-  TK_CUDA(cudaMalloc(&d_sl, n_slices * sizeof(tk_slice)));
-  TK_CUDA(cudaMalloc(&d_bt, std::max(1, n_bt) * 4));
-  TK_CUDA(cudaMalloc(&d_work, std::max(1, n_work) * sizeof(AttnWork)));
-  TK_CUDA(cudaMalloc(&d_qb, std::max(1, n_qb) * sizeof(AttnQBlock)));
-  TK_CUDA(cudaMalloc(&d_part, attn_partial_bytes(n_heads, head_dim)));
-  TK_CUDA(cudaMemcpy(d_sl, slices, n_slices * sizeof(tk_slice), cudaMemcpyHostToDevice));
-  TK_CUDA(cudaMemcpy(d_bt, block_tables, n_bt * 4, cudaMemcpyHostToDevice));
-  TK_CUDA(cudaMemcpy(d_work, work.data(), n_work * sizeof(AttnWork), cudaMemcpyHostToDevice));
-  TK_CUDA(cudaMemcpy(d_qb, qbs.data(), n_qb * sizeof(AttnQBlock), cudaMemcpyHostToDevice));
+  std::vector<void*> dev;
+  auto upload = [&](const void* src, size_t bytes) -> void* {
+    void* d = nullptr;
+    if (cudaMalloc(&d, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+    dev.push_back(d);
+    if (src && bytes && cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return d;
+  };
+  struct Freer {
+    std::vector<void*>& v;
+    ~Freer() { for (void* p : v) cudaFree(p); }
+  } freer{dev};
+  void* d_sl = upload(slices, n_slices * sizeof(tk_slice));
+  void* d_bt = upload(block_tables, std::max(1, n_bt) * 4);
+  void* d_part = upload(nullptr, attn_partial_bytes(n_heads, head_dim));
+  TK_CHECK(d_sl && d_bt && d_part, TK_ECUDA, "tk_chunk_attention: device staging");
+  FaPlan fa{};
+  void *d_pairs = nullptr, *d_units = nullptr, *d_groups = nullptr, *d_off = nullptr;
+  void *d_work = nullptr, *d_qb = nullptr;
+  int n_qb = 0, n_work = 0;
+  bool any_split = false;
+  if (tc_attn) {
+    const int pcap = n_slices + n_tokens / 256 + 1;
+    const int ucap = pcap * n_heads + kNumSMs + 1;
+    std::vector<FaPair> pairs(pcap);
+    std::vector<FaUnit> units(ucap);
+    std::vector<FaGroup> groups(pcap * n_heads);
+    std::vector<int32_t> off(kNumSMs + 1);
+    TK_CHECK(build_fa_plan(slices, n_slices, n_heads, kNumSMs, &fa, pairs.data(), pcap,
+                           units.data(), ucap, groups.data(), pcap * n_heads, off.data(),
+                           kNumSMs + 1) == 0,
+             TK_EINVAL, "tk_chunk_attention: attention plan overflow");
+    d_pairs = upload(pairs.data(), pairs.size() * sizeof(FaPair));
+    d_units = upload(units.data(), units.size() * sizeof(FaUnit));
+    d_groups = upload(groups.data(), groups.size() * sizeof(FaGroup));
+    d_off = upload(off.data(), off.size() * 4);
+    TK_CHECK(d_pairs && d_units && d_groups && d_off, TK_ECUDA, "tk_chunk_attention: staging");
+  } else {
+    const int qcap = n_slices + n_tokens / 128 + 1;
+    std::vector<AttnQBlock> qbs(qcap);
+    std::vector<AttnWork> work(qcap + kAttnMaxSplitSlots);
+    n_work = build_attn_work(slices, n_slices, n_heads, qbs.data(), qcap, work.data(),
+                             static_cast<int>(work.size()), &n_qb, 64);
+    TK_CHECK(n_work >= 0, TK_EINVAL, "tk_chunk_attention: work list");
+    for (int k = 0; k < n_qb; ++k) any_split |= qbs[k].n_splits > 1;
+    d_work = upload(work.data(), std::max(1, n_work) * sizeof(AttnWork));
+    d_qb = upload(qbs.data(), std::max(1, n_qb) * sizeof(AttnQBlock));
+    TK_CHECK(d_work && d_qb, TK_ECUDA, "tk_chunk_attention: staging");
+  }
   KvGeom g{n_layers, n_heads, head_dim, page_tokens};
-  int rc;
+  int rc = TK_OK;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (iters > 1) {
+    TK_CUDA(cudaEventCreate(&ev0));
+    TK_CUDA(cudaEventCreate(&ev1));
+  }
+  for (int it = 0; it < std::max(1, iters) && rc == TK_OK; ++it) {
+  if (iters > 1 && it == 1) TK_CUDA(cudaEventRecord(ev0, s));
   if (tc_attn) {
     // the pool extent: enough pages to cover every page id referenced
     int max_page = 0;
     for (int i = 0; i < n_bt; ++i) max_page = std::max(max_page, block_tables[i]);
-    rc = launch_chunk_attention_tc(
+    rc = launch_chunk_attention_fa(
         static_cast<const __nv_bfloat16*>(q), n_tokens, q_stride, static_cast<__nv_bfloat16*>(o),
-        static_cast<const __nv_bfloat16*>(kv_pool), max_page + 1, g, layer,
-        static_cast<AttnWork*>(d_work), n_work, static_cast<AttnQBlock*>(d_qb), n_qb, any_split,
+        static_cast<const __nv_bfloat16*>(kv_pool), max_page + 1, g, layer, fa,
+        static_cast<FaPair*>(d_pairs), static_cast<FaUnit*>(d_units),
+        static_cast<FaGroup*>(d_groups), static_cast<int32_t*>(d_off),
         static_cast<tk_slice*>(d_sl), static_cast<int32_t*>(d_bt), scale,
         static_cast<float*>(d_part), s);
   } else {
@@ -1158,13 +1217,39 @@ int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_
         n_work, static_cast<AttnQBlock*>(d_qb), n_qb, any_split, static_cast<tk_slice*>(d_sl),
         static_cast<int32_t*>(d_bt), scale, static_cast<float*>(d_part), s);
   }
+  }
+  if (iters > 1 && rc == TK_OK) {
+    // launches 2..iters back to back (the first one warms up)
+    TK_CUDA(cudaEventRecord(ev1, s));
+    TK_CUDA(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    TK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    if (avg_us) *avg_us = ms * 1e3f / static_cast<float>(iters - 1);
+  }
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
   TK_CUDA(cudaStreamSynchronize(s));
-  cudaFree(d_sl);
-  cudaFree(d_bt);
-  cudaFree(d_work);
-  cudaFree(d_qb);
-  cudaFree(d_part);
   return rc;
+}
+
+int tk_chunk_attention(const void* q, int32_t q_stride, void* o, const void* kv_pool,
+                       int32_t layer, int32_t n_layers, int32_t n_heads, int32_t head_dim,
+                       int32_t page_tokens, const tk_slice* slices, int32_t n_slices,
+                       const int32_t* block_tables, int32_t n_tokens, float scale, void* stream) {
+  return chunk_attention_impl(q, q_stride, o, kv_pool, layer, n_layers, n_heads, head_dim,
+                              page_tokens, slices, n_slices, block_tables, n_tokens, scale, stream,
+                              1, nullptr);
+}
+
+int tk_chunk_attention_timed(const void* q, int32_t q_stride, void* o, const void* kv_pool,
+                             int32_t layer, int32_t n_layers, int32_t n_heads, int32_t head_dim,
+                             int32_t page_tokens, const tk_slice* slices, int32_t n_slices,
+                             const int32_t* block_tables, int32_t n_tokens, float scale,
+                             void* stream, int32_t iters, float* avg_us) {
+  TK_CHECK(iters >= 2 && avg_us, TK_EINVAL, "tk_chunk_attention_timed: iters >= 2, avg_us");
+  return chunk_attention_impl(q, q_stride, o, kv_pool, layer, n_layers, n_heads, head_dim,
+                              page_tokens, slices, n_slices, block_tables, n_tokens, scale, stream,
+                              iters, avg_us);
 }
 
 int tk_event_elapsed(tk_event* a, tk_event* b, int64_t* elapsed_ns) {

@@ -84,13 +84,36 @@ int build_attn_work(const tk_slice* slices, int n_slices, int n_heads, AttnQBloc
                     AttnWork* items, int icap, int* n_qblocks, int block_keys);
 int launch_attn_combine(__nv_bfloat16* o, const AttnQBlock* qblocks, int n_qblocks, int n_heads,
                         int head_dim, float* partial, cudaStream_t s);
-// tcgen05 / TMEM chunk attention (head_dim 128, 128-key blocks).
-int launch_chunk_attention_tc(const __nv_bfloat16* qkv, int q_rows, int q_stride,
+// tcgen05 / TMEM chunk attention (head_dim 128): persistent CTAs over a
+// stream-K split of (head, query-tile pair, 128-key block) space.
+constexpr int kFaMaxPieces = 2 * 148;  // split pieces per launch (<= 2 per CTA boundary)
+struct FaPair {                        // two 128-row query tiles of one slice
+  int32_t slice, row0, pos0;           // chunk row / request position of tile 0's first row
+  int32_t nrows0, nrows1;              // rows in tile 0 / tile 1 (0: lone tile)
+  int32_t nblk;                        // 128-key blocks up to tile 1's (or lone tile's) last row
+};
+struct FaUnit {
+  int32_t pair, head, kb0, kb1;        // key blocks [kb0, kb1) of this (pair, head)
+  int32_t piece;                       // partial slot (-1: the whole (pair, head), written directly)
+};
+struct FaGroup {
+  int32_t first_piece, n_pieces;       // pieces of one (pair, head)
+};
+struct FaPlan {
+  int n_pairs, n_units, n_ctas, n_pieces;
+};
+// Host-side plan; arrays are caller-provided with capacities.  0 / -1 (overflow).
+int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_ctas, FaPlan* plan,
+                  FaPair* pairs, int pcap, FaUnit* units, int ucap, FaGroup* groups, int gcap,
+                  int32_t* cta_off, int ocap);
+int64_t fa_partial_bytes();
+int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride,
                               __nv_bfloat16* o, const __nv_bfloat16* pool, int pool_pages,
-                              KvGeom g, int layer, const AttnWork* work, int n_work,
-                              const AttnQBlock* qblocks, int n_qblocks, bool any_split,
-                              const tk_slice* slices_dev, const int32_t* bt_dev, float scale,
-                              float* partial, cudaStream_t s);
+                              KvGeom g, int layer, const FaPlan& plan, const FaPair* pairs_dev,
+                              const FaUnit* units_dev, const FaGroup* groups_dev,
+                              const int32_t* cta_off_dev, const tk_slice* slices_dev,
+                              const int32_t* bt_dev, float scale, float* partial,
+                              cudaStream_t s);
 // true: use the tcgen05 attention for this head_dim (TK_ATTN_MMA_SYNC=1 forces mma.sync)
 bool use_tc_attention(int head_dim);
 int64_t attn_partial_bytes(int n_heads, int head_dim);

@@ -85,6 +85,10 @@ _SIGNATURES = {
     "tk_chunk_attention": ([_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                             C.c_int32, C.POINTER(tk_slice), C.c_int32, _I32P, C.c_int32,
                             C.c_float, _P], C.c_int),
+    "tk_chunk_attention_timed": ([_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32,
+                                  C.c_int32, C.c_int32, C.POINTER(tk_slice), C.c_int32, _I32P,
+                                  C.c_int32, C.c_float, _P, C.c_int32, C.POINTER(C.c_float)],
+                                 C.c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -476,3 +480,18 @@ def chunk_attention(q, q_stride, pool, layer, n_layers, n_heads, head_dim, slice
         sl, len(slices), i32(block_tables), n, scale if scale else head_dim ** -0.5,
         _stream(stream)), "tk_chunk_attention")
     return o
+
+
+def chunk_attention_timed(q, q_stride, pool, layer, n_layers, n_heads, head_dim, slices,
+                          block_tables, iters=20, page_tokens=16, scale=None, stream=None):
+    """(o, mean device microseconds per launch) -- microbenchmarks only."""
+    import torch
+    n = sum(s[1] for s in slices)
+    o = torch.empty((n, n_heads * head_dim), dtype=torch.bfloat16, device=q.device)
+    sl = (tk_slice * len(slices))(*[tk_slice(*s) for s in slices])
+    us = C.c_float()
+    check(load().tk_chunk_attention_timed(
+        _ptr(q), q_stride, _ptr(o), _ptr(pool), layer, n_layers, n_heads, head_dim, page_tokens,
+        sl, len(slices), i32(block_tables), n, scale if scale else head_dim ** -0.5,
+        _stream(stream), iters, C.byref(us)), "tk_chunk_attention_timed")
+    return o, us.value

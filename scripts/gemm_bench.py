@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--m", type=int, nargs="*", default=[512])
     ap.add_argument("--shapes", nargs="*", default=list(SHAPES))
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--epi", default=None, choices=["bf16", "f32", "resid"],
+                    help="override the shape's epilogue (isolates epilogue cost)")
     args = ap.parse_args()
     native.load()
     peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
@@ -34,6 +36,9 @@ def main():
     for M in args.m:
         for name in args.shapes:
             N, K, epi = SHAPES[name]
+            if args.epi:
+                epi = {"bf16": native.EPI_BF16, "f32": native.EPI_F32,
+                       "resid": native.EPI_F32_BIAS_RESID}[args.epi]
             a = torch.randn(M, K, device="cuda").bfloat16()
             b = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
             bias = torch.zeros(N, device="cuda").bfloat16()
@@ -58,7 +63,7 @@ def main():
                 times.append(s.elapsed_time(e))
             ms = sorted(times)[len(times) // 2]
             tf = 2 * M * N * K / (ms / 1e3) / 1e12
-            print(json.dumps({"shape": name, "M": M, "N": N, "K": K, "median_us": round(ms * 1e3, 2),
+            print(json.dumps({"shape": name, "epi": epi, "M": M, "N": N, "K": K, "median_us": round(ms * 1e3, 2),
                               "tflops": round(tf, 1),
                               "frac_burst": round(tf / peak["bf16_tflops"], 3)}))
 

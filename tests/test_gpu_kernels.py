@@ -168,6 +168,33 @@ def test_chunk_attention_mixed_slices():
         row += n
 
 
+@pytest.mark.parametrize("prefix,n,H", [(0, 512, 40), (3000, 512, 40), (7680, 512, 8),
+                                        (130, 77, 40), (256, 300, 3)])
+def test_chunk_attention_long_prefix_pieces(prefix, n, H):
+    """One slice over a long paged prefix: the stream-K plan cuts (head, tile pair)
+    work into pieces merged by the combine kernel; unaligned starts and lone tiles."""
+    g = torch.Generator(device="cuda").manual_seed(prefix + n)
+    L, D, pt = 2, 128, 16
+    n_pages = (prefix + n + pt - 1) // pt
+    pool = _pool(n_pages, L, H, D, pt, g)
+    bt = torch.randperm(n_pages, generator=torch.Generator().manual_seed(3)).tolist()
+    slices = [(prefix, n, 0, n_pages, 1)]
+    qkv = torch.randn(n, 3 * H * D, device="cuda", generator=g).bfloat16()
+    o = native.chunk_attention(qkv, 3 * H * D, pool, 0, L, H, D, slices, bt, pt)
+    torch.cuda.synchronize()
+    heads = sorted({0, H // 2, H - 1})
+    K, V = _gather_kv(pool, 0, bt, prefix + n, pt)
+    q = qkv[:, :H * D].float().view(n, H, D).transpose(0, 1)
+    qpos = torch.arange(prefix, prefix + n, device="cuda")[:, None]
+    kpos = torch.arange(0, prefix + n, device="cuda")[None, :]
+    for h in heads:
+        sc = (q[h] @ K[h].t()) * D ** -0.5
+        sc = sc.masked_fill(kpos > qpos, float("-inf"))
+        ref = torch.softmax(sc, -1) @ V[h]
+        err = (o[:, h * D:(h + 1) * D].float() - ref).abs().max().item()
+        assert err < 2e-2, (h, err)
+
+
 def test_gemm_shared_workspace_across_shapes():
     """One workspace serves every GEMM shape of a layer (as in the runtime)."""
     import ctypes
