@@ -653,12 +653,27 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
 // m-groups) form a cluster and every B half is loaded as two 64-row slices
 // multicast to the CTAs of both pairs that hold that half, so weights are
 // still fetched once per GEMM.
-template <int EPI, int CS>
+//
+// BN (tile width) is 256, or 160 for N=5120-class GEMMs (O-proj, FC2 at
+// M=512): 32 clusters of 512x160 cover N in exactly one wave, so no tile is
+// split and there is no stream-K fixup; 256-wide tiles would leave 40% of the
+// SMs idle or need a split-K exchange per tile.
+template <int BN>
+struct PairCfg {
+  static constexpr int A_BYTES = 128 * 64 * 2;
+  static constexpr int BH_BYTES = (BN / 2) * 64 * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
+  static constexpr int STAGES = (220 * 1024 - 2048) / STAGE_BYTES > 8 ? 8 : (220 * 1024 - 2048) / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 256 + 1024;
+};
+
+template <int EPI, int CS, int BN>
 __global__ void __launch_bounds__(192, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b, const GemmArgs p) {
-  constexpr int BM = 128, BN = 256, BK = 64;
-  constexpr int STAGES = 6;
+  constexpr int BM = 128, BK = 64;
+  static_assert(BN % 32 == 0 && BN <= 256 && (BN / 2 / (CS / 2)) % 8 == 0, "pair tile width");
+  constexpr int STAGES = PairCfg<BN>::STAGES;
   constexpr int A_BYTES = BM * BK * 2;        // own 128 rows
   constexpr int BH_BYTES = (BN / 2) * BK * 2;  // own half of the B tile
   constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
@@ -760,7 +775,7 @@ __global__ void __launch_bounds__(192, 1)
         const int nkb = static_cast<int>(seg_end - i);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * 256;
         for (int k = 0; k < nkb; ++k) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -799,9 +814,19 @@ __global__ void __launch_bounds__(192, 1)
       const int row = m_idx * BM + row_in_tile;
       const int col_base = n_idx * BN;
       const int contrib = owner_of(tile_first + kbs - 1, T, G) - owner_of(tile_first, T, G) + 1;
+      if constexpr (EPI == EPI_F32_BIAS_RESID) {
+        // pull this row's residual segment into L2 while the MMAs run: the
+        // epilogue's read-modify-write then waits on L2, not HBM
+        if (row < p.M) {
+          const float* seg = reinterpret_cast<const float*>(p.C) + static_cast<size_t>(row) * p.N + col_base;
+#pragma unroll
+          for (int c = 0; c < BN; c += 32)
+            if (col_base + c < p.N) prefetch_l2(seg + c);
+        }
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + ((quarter * 32) << 16) + acc * BN;
+      const uint32_t t_row = tmem_base + ((quarter * 32) << 16) + acc * 256;
       auto release_tmem = [&]() {
         tc_fence_before();
         __syncwarp();
@@ -890,7 +915,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
 }
 
-constexpr int kPairSmemBytes = 6 * (128 * 64 * 2 + 128 * 64 * 2) + 256 + 1024;
+
 
 // ------------------------------------------------------------------ host side
 
@@ -950,6 +975,7 @@ int make_tmap_kv_pages(CUtensorMap* map, const void* pool, uint64_t blocks, uint
 }
 
 static int pick_bn(int N) { return N >= 1024 ? 256 : 128; }
+constexpr int kNarrowBN = 160;  // pair-kernel tile width for one-wave N=5120-class GEMMs
 
 // Co-resident clusters of size cs for the BN variant (queried once per variant).
 static int max_clusters_for(int bn, int cs);
@@ -1027,15 +1053,28 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
   pl.bn = pick_bn(N);
   pl.tiles_m = (M + 127) / 128;
   pl.pair = pl.bn == 256 && pl.tiles_m % 2 == 0 && getenv("TK_NO_PAIR") == nullptr;
-  pl.tiles_n = (N + pl.bn - 1) / pl.bn;
-  pl.kbs = K / 64;
   pl.cs = pl.tiles_m % 4 == 0 ? 4 : (pl.tiles_m % 2 == 0 ? 2 : 1);
-  pl.total_iters = static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
   if (pl.pair && pl.cs == 1) pl.cs = 2;
   int clusters = pl.pair ? max_pair_clusters(pl.cs) : max_clusters_for(pl.bn, pl.cs);
   if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / pl.cs));
+  bool one_wave = false;
+  // (for long K the 256-wide stream-K schedule wins: narrow tiles re-read A
+  // from L2 for every 160 columns, and the fixup is amortised over many k-blocks)
+  if (pl.pair && K <= 8192 && getenv("TK_NO_NARROW") == nullptr) {
+    // narrow tiles when they cover the whole GEMM in one wave of clusters
+    const int groups_m = pl.tiles_m / pl.cs;
+    const int tn = (N + kNarrowBN - 1) / kNarrowBN;
+    if (tn * groups_m <= clusters && 4 * tn * groups_m >= 3 * clusters) {
+      pl.bn = kNarrowBN;
+      one_wave = true;
+    }
+  }
+  pl.tiles_n = (N + pl.bn - 1) / pl.bn;
+  pl.kbs = K / 64;
+  pl.total_iters = static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
+  if (one_wave) clusters = static_cast<int>(pl.total_iters / pl.kbs);  // one tile per cluster
   clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, pl.total_iters / 4)));
-  if (max_ctas <= 0) clusters = pick_clusters(pl.total_iters, pl.kbs, clusters);
+  if (max_ctas <= 0 && !one_wave) clusters = pick_clusters(pl.total_iters, pl.kbs, clusters);
   pl.clusters = clusters;
   // most CTAs (clusters) sharing one tile, over all cluster tiles
   const long long ctiles = pl.total_iters / pl.kbs;
@@ -1086,20 +1125,20 @@ static int skinny_epi(const CUtensorMap& tw, const CUtensorMap& tx, const GemmAr
   return TK_EINVAL;
 }
 
-template <int EPI, int CS>
+template <int EPI, int CS, int BN>
 static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                        int clusters, cudaStream_t stream) {
-  auto kern = gemm_pair_kernel<EPI, CS>;
+  auto kern = gemm_pair_kernel<EPI, CS, BN>;
   static bool configured = false;
   if (!configured) {
     TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kPairSmemBytes));
+                                 PairCfg<BN>::SMEM));
     configured = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * CS);
   cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = kPairSmemBytes;
+  cfg.dynamicSmemBytes = PairCfg<BN>::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1113,15 +1152,15 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   return TK_OK;
 }
 
-template <int CS>
+template <int CS, int BN>
 static int pair_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int clusters,
                     cudaStream_t s) {
   switch (a.epi) {
-    case EPI_BF16: return launch_pair<EPI_BF16, CS>(ta, tb, a, clusters, s);
-    case EPI_BF16_BIAS: return launch_pair<EPI_BF16_BIAS, CS>(ta, tb, a, clusters, s);
-    case EPI_BF16_BIAS_RELU: return launch_pair<EPI_BF16_BIAS_RELU, CS>(ta, tb, a, clusters, s);
-    case EPI_F32_BIAS_RESID: return launch_pair<EPI_F32_BIAS_RESID, CS>(ta, tb, a, clusters, s);
-    case EPI_F32: return launch_pair<EPI_F32, CS>(ta, tb, a, clusters, s);
+    case EPI_BF16: return launch_pair<EPI_BF16, CS, BN>(ta, tb, a, clusters, s);
+    case EPI_BF16_BIAS: return launch_pair<EPI_BF16_BIAS, CS, BN>(ta, tb, a, clusters, s);
+    case EPI_BF16_BIAS_RELU: return launch_pair<EPI_BF16_BIAS_RELU, CS, BN>(ta, tb, a, clusters, s);
+    case EPI_F32_BIAS_RESID: return launch_pair<EPI_F32_BIAS_RESID, CS, BN>(ta, tb, a, clusters, s);
+    case EPI_F32: return launch_pair<EPI_F32, CS, BN>(ta, tb, a, clusters, s);
   }
   set_error("unknown gemm epilogue");
   return TK_EINVAL;
@@ -1129,8 +1168,8 @@ static int pair_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs
 
 template <int CS>
 static int query_pair_clusters() {
-  auto kern = gemm_pair_kernel<EPI_BF16, CS>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmemBytes) !=
+  auto kern = gemm_pair_kernel<EPI_BF16, CS, 256>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256>::SMEM) !=
       cudaSuccess) {
     cudaGetLastError();
     return kNumSMs / CS;
@@ -1138,7 +1177,7 @@ static int query_pair_clusters() {
   cudaLaunchConfig_t q{};
   q.gridDim = dim3(kNumSMs / CS * CS);
   q.blockDim = dim3(192);
-  q.dynamicSmemBytes = kPairSmemBytes;
+  q.dynamicSmemBytes = PairCfg<256>::SMEM;
   cudaLaunchAttribute qa[1];
   qa[0].id = cudaLaunchAttributeClusterDimension;
   qa[0].val.clusterDim.x = CS;
@@ -1324,10 +1363,14 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   if (pl.pair) {
     // each CTA loads 64-row (CS=4) or 128-row (CS=2) slices of its B half
     CUtensorMap tb;
-    rc = make_tmap_kmajor(&tb, B, N, K, 128 / (pl.cs / 2));
+    rc = make_tmap_kmajor(&tb, B, N, K, pl.bn / 2 / (pl.cs / 2));
     if (rc) return rc;
-    if (pl.cs == 4) return pair_epi<4>(ta, tb, a, pl.clusters, stream);
-    return pair_epi<2>(ta, tb, a, pl.clusters, stream);
+    if (pl.bn == kNarrowBN) {
+      if (pl.cs == 4) return pair_epi<4, kNarrowBN>(ta, tb, a, pl.clusters, stream);
+      return pair_epi<2, kNarrowBN>(ta, tb, a, pl.clusters, stream);
+    }
+    if (pl.cs == 4) return pair_epi<4, 256>(ta, tb, a, pl.clusters, stream);
+    return pair_epi<2, 256>(ta, tb, a, pl.clusters, stream);
   }
   if (pl.bn == 256) return dispatch_cs<256>(B, N, K, ta, a, pl.clusters, stream);
   return dispatch_cs<128>(B, N, K, ta, a, pl.clusters, stream);

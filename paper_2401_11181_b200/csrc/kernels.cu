@@ -92,19 +92,29 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 constexpr int kNormThreads = 256;
 constexpr int kNormMaxPer = 32;  // cols <= 8192
 
-template <bool kRms>
+// kAdd: x += delta (bf16 output of the preceding O-proj / FC2 GEMM, bias
+// included) is applied first and written back, so the residual stream stays
+// fp32 while those GEMMs store bf16 instead of read-modify-writing fp32.
+template <bool kRms, bool kAdd>
 __global__ void __launch_bounds__(kNormThreads)
-    norm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-                const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y, int cols,
-                float eps) {
+    norm_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+                const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ b,
+                __nv_bfloat16* __restrict__ y, int cols, float eps) {
   __shared__ float red[kNormThreads / 32];
-  const float* xr = x + static_cast<size_t>(blockIdx.x) * cols;
+  float* xr = x + static_cast<size_t>(blockIdx.x) * cols;
   __nv_bfloat16* yr = y + static_cast<size_t>(blockIdx.x) * cols;
   float v[kNormMaxPer];
   int n = 0;
   float s = 0.f;
   for (int c = threadIdx.x * 4; c < cols; c += kNormThreads * 4, n += 4) {
     float4 q = *reinterpret_cast<const float4*>(xr + c);
+    if constexpr (kAdd) {
+      const uint2 d = *reinterpret_cast<const uint2*>(delta + static_cast<size_t>(blockIdx.x) * cols + c);
+      const float2 d01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d.x));
+      const float2 d23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d.y));
+      q.x += d01.x; q.y += d01.y; q.z += d23.x; q.w += d23.y;
+      *reinterpret_cast<float4*>(xr + c) = q;
+    }
     v[n] = q.x; v[n + 1] = q.y; v[n + 2] = q.z; v[n + 3] = q.w;
     s += q.x + q.y + q.z + q.w;
   }
@@ -134,38 +144,53 @@ __global__ void __launch_bounds__(kNormThreads)
 
 int launch_layernorm(const float* x, const __nv_bfloat16* w, const __nv_bfloat16* b,
                      __nv_bfloat16* y, int rows, int cols, float eps, cudaStream_t s) {
-  TK_CHECK(cols % 4 == 0 && cols <= kNormThreads * kNormMaxPer, TK_EINVAL,
-           "layernorm: cols must be a multiple of 4 and <= 8192");
-  if (rows == 0) return TK_OK;
-  norm_kernel<false><<<rows, kNormThreads, 0, s>>>(x, w, b, y, cols, eps);
-  TK_CUDA(cudaGetLastError());
-  note_launch();
-  return TK_OK;
+  return launch_add_norm(const_cast<float*>(x), nullptr, w, b, y, rows, cols, eps, false, s);
 }
 
 int launch_rmsnorm(const float* x, const __nv_bfloat16* w, __nv_bfloat16* y, int rows, int cols,
                    float eps, cudaStream_t s) {
+  return launch_add_norm(const_cast<float*>(x), nullptr, w, nullptr, y, rows, cols, eps, true, s);
+}
+
+int launch_add_norm(float* x, const __nv_bfloat16* delta, const __nv_bfloat16* w,
+                    const __nv_bfloat16* b, __nv_bfloat16* y, int rows, int cols, float eps,
+                    bool rms, cudaStream_t s) {
   TK_CHECK(cols % 4 == 0 && cols <= kNormThreads * kNormMaxPer, TK_EINVAL,
-           "rmsnorm: cols must be a multiple of 4 and <= 8192");
+           "norm: cols must be a multiple of 4 and <= 8192");
   if (rows == 0) return TK_OK;
-  norm_kernel<true><<<rows, kNormThreads, 0, s>>>(x, w, nullptr, y, cols, eps);
+  if (rms) {
+    if (delta) norm_kernel<true, true><<<rows, kNormThreads, 0, s>>>(x, delta, w, nullptr, y, cols, eps);
+    else norm_kernel<true, false><<<rows, kNormThreads, 0, s>>>(x, nullptr, w, nullptr, y, cols, eps);
+  } else {
+    if (delta) norm_kernel<false, true><<<rows, kNormThreads, 0, s>>>(x, delta, w, b, y, cols, eps);
+    else norm_kernel<false, false><<<rows, kNormThreads, 0, s>>>(x, nullptr, w, b, y, cols, eps);
+  }
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;
 }
 
-__global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows,
-                                   int cols, float* __restrict__ out) {
-  const float* src = x + static_cast<size_t>(rows[blockIdx.x]) * cols;
+__global__ void gather_rows_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+                                   const int32_t* __restrict__ rows, int cols,
+                                   float* __restrict__ out) {
+  const size_t r = static_cast<size_t>(rows[blockIdx.x]) * cols;
   float* dst = out + static_cast<size_t>(blockIdx.x) * cols;
-  for (int c = threadIdx.x * 4; c < cols; c += blockDim.x * 4)
-    *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
+  for (int c = threadIdx.x * 4; c < cols; c += blockDim.x * 4) {
+    float4 q = *reinterpret_cast<const float4*>(x + r + c);
+    if (delta) {
+      const uint2 d = *reinterpret_cast<const uint2*>(delta + r + c);
+      const float2 d01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d.x));
+      const float2 d23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d.y));
+      q.x += d01.x; q.y += d01.y; q.z += d23.x; q.w += d23.y;
+    }
+    *reinterpret_cast<float4*>(dst + c) = q;
+  }
 }
 
 int launch_gather_rows_f32(const float* x, const int32_t* rows, int n, int cols, float* out,
-                           cudaStream_t s) {
+                           cudaStream_t s, const __nv_bfloat16* delta) {
   if (n == 0) return TK_OK;
-  gather_rows_kernel<<<n, 256, 0, s>>>(x, rows, cols, out);
+  gather_rows_kernel<<<n, 256, 0, s>>>(x, delta, rows, cols, out);
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;

@@ -277,6 +277,7 @@ struct tk_instance {
   cudaStream_t s_compute = nullptr, s_copy = nullptr, s_pred = nullptr;
   // scratch
   float* resid = nullptr;
+  __nv_bfloat16* delta = nullptr;  // pending bf16 residual update (O-proj / FC2 output)
   __nv_bfloat16 *xn = nullptr, *qkv = nullptr, *attn = nullptr, *ffn = nullptr;
   float* logits = nullptr;
   int max_emit = 0;
@@ -405,9 +406,12 @@ static int run_layer(tk_instance* inst, int layer, int n, const TokenMeta* meta_
   const bool opt = m.arch == TK_ARCH_OPT;
   const int hi = m.hidden;
   int rc;
-  rc = profiled(inst, s, PK_OTHER, 0, nn * h * 6, [&] {
-    return opt ? launch_layernorm(inst->resid, L.ln1_w, L.ln1_b, inst->xn, n, hi, m.norm_eps, s)
-               : launch_rmsnorm(inst->resid, L.ln1_w, inst->xn, n, hi, m.norm_eps, s);
+  // The residual stream is fp32; O-proj and FC2 store their bf16 output
+  // (bias included) in inst->delta and the next norm adds it in.
+  const __nv_bfloat16* pending = layer > 0 ? inst->delta : nullptr;
+  rc = profiled(inst, s, PK_OTHER, 0, nn * h * (pending ? 12 : 6), [&] {
+    return launch_add_norm(inst->resid, pending, L.ln1_w, opt ? L.ln1_b : nullptr, inst->xn, n,
+                           hi, m.norm_eps, !opt, s);
   });
   if (rc) return rc;
   rc = profiled(inst, s, PK_QKV, 2 * nn * 3 * h * h, (3 * h * h + nn * 4 * h) * 2, [&] {
@@ -422,14 +426,14 @@ static int run_layer(tk_instance* inst, int layer, int n, const TokenMeta* meta_
   if (rc) return rc;
   rc = profiled(inst, s, PK_ATTN, attn_flops, attn_bytes, attention_fn);
   if (rc) return rc;
-  rc = profiled(inst, s, PK_O, 2 * nn * h * h, (h * h + nn * h) * 2 + nn * h * 8, [&] {
-    return gemm_bf16(inst->attn, L.o_w, inst->resid, L.o_b, n, hi, hi, EPI_F32_BIAS_RESID,
+  rc = profiled(inst, s, PK_O, 2 * nn * h * h, (h * h + nn * h) * 2 + nn * h * 2, [&] {
+    return gemm_bf16(inst->attn, L.o_w, inst->delta, L.o_b, n, hi, hi, EPI_BF16_BIAS,
                      inst->gemm_ws, inst->gemm_ws_bytes, s);
   });
   if (rc) return rc;
-  rc = profiled(inst, s, PK_OTHER, 0, nn * h * 6, [&] {
-    return opt ? launch_layernorm(inst->resid, L.ln2_w, L.ln2_b, inst->xn, n, hi, m.norm_eps, s)
-               : launch_rmsnorm(inst->resid, L.ln2_w, inst->xn, n, hi, m.norm_eps, s);
+  rc = profiled(inst, s, PK_OTHER, 0, nn * h * 12, [&] {
+    return launch_add_norm(inst->resid, inst->delta, L.ln2_w, opt ? L.ln2_b : nullptr, inst->xn,
+                           n, hi, m.norm_eps, !opt, s);
   });
   if (rc) return rc;
   const double up = opt ? f : 2 * f;
@@ -448,8 +452,8 @@ static int run_layer(tk_instance* inst, int layer, int n, const TokenMeta* meta_
   }
   const __nv_bfloat16* ffn_act =
       opt ? inst->ffn : inst->ffn + static_cast<size_t>(n) * 2 * m.ffn;
-  rc = profiled(inst, s, PK_FC2, 2 * nn * h * f, (h * f + nn * f) * 2 + nn * h * 8, [&] {
-    return gemm_bf16(ffn_act, L.fc2_w, inst->resid, L.fc2_b, n, hi, m.ffn, EPI_F32_BIAS_RESID,
+  rc = profiled(inst, s, PK_FC2, 2 * nn * h * f, (h * f + nn * f) * 2 + nn * h * 2, [&] {
+    return gemm_bf16(ffn_act, L.fc2_w, inst->delta, L.fc2_b, n, hi, m.ffn, EPI_BF16_BIAS,
                      inst->gemm_ws, inst->gemm_ws_bytes, s);
   });
   return rc;
@@ -462,7 +466,9 @@ static int run_head(tk_instance* inst, int n_rows, const int32_t* rows_dev, int3
   Weights* w = inst->w;
   int rc;
   float* gathered = reinterpret_cast<float*>(inst->qkv);  // qkv scratch is free here
-  rc = launch_gather_rows_f32(inst->resid, rows_dev, n_rows, m.hidden, gathered, s);
+  // the last layer's FC2 output is still pending in inst->delta
+  rc = launch_gather_rows_f32(inst->resid, rows_dev, n_rows, m.hidden, gathered, s,
+                              m.n_layers > 0 ? inst->delta : nullptr);
   if (rc) return rc;
   rc = m.arch == TK_ARCH_OPT
            ? launch_layernorm(gathered, w->fln_w, w->fln_b, inst->xn, n_rows, m.hidden, m.norm_eps, s)
@@ -542,6 +548,7 @@ int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed
   const int64_t rows = max_chunk;
   const int ffn_cols = m.arch == TK_ARCH_OPT ? m.ffn : 3 * m.ffn;
   TK_CUDA(cudaMalloc(&inst->resid, rows * m.hidden * 4));
+  TK_CUDA(cudaMalloc(&inst->delta, rows * m.hidden * 2));
   TK_CUDA(cudaMalloc(&inst->xn, rows * m.hidden * 2));
   // qkv scratch doubles as the fp32 gather buffer of the head
   TK_CUDA(cudaMalloc(&inst->qkv, rows * std::max<int64_t>(3 * m.hidden * 2, m.hidden * 4)));
@@ -596,6 +603,7 @@ int tk_instance_destroy(tk_instance* inst) {
   }
   cudaFree(inst->pool);
   cudaFree(inst->resid);
+  cudaFree(inst->delta);
   cudaFree(inst->xn);
   cudaFree(inst->qkv);
   cudaFree(inst->attn);

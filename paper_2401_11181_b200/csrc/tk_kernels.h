@@ -58,8 +58,13 @@ int launch_layernorm(const float* x, const __nv_bfloat16* w, const __nv_bfloat16
                      __nv_bfloat16* y, int rows, int cols, float eps, cudaStream_t s);
 int launch_rmsnorm(const float* x, const __nv_bfloat16* w, __nv_bfloat16* y, int rows, int cols,
                    float eps, cudaStream_t s);
+// out[i] = x[rows[i]] (+ delta[rows[i]] when given: the residual's pending bf16 update)
 int launch_gather_rows_f32(const float* x, const int32_t* rows, int n, int cols, float* out,
-                           cudaStream_t s);
+                           cudaStream_t s, const __nv_bfloat16* delta = nullptr);
+// x += delta (written back), then y = LayerNorm / RMSNorm(x); delta may be null.
+int launch_add_norm(float* x, const __nv_bfloat16* delta, const __nv_bfloat16* w,
+                    const __nv_bfloat16* b, __nv_bfloat16* y, int rows, int cols, float eps,
+                    bool rms, cudaStream_t s);
 // qkv [n, 3*H*D] bf16 (q scaled in place by q_scale) -> K,V into pages.
 int launch_kv_write(__nv_bfloat16* qkv, const TokenMeta* meta, int n, __nv_bfloat16* pool,
                     KvGeom g, int layer, float q_scale, int rope, float rope_theta,

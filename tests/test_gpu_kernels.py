@@ -40,6 +40,10 @@ def _rel_err(x, ref):
     (16, 5120, 20480),   # skinny NB=16, long K (many stream-K contributors)
     (100, 20480, 5120),  # skinny NB=128
     (128, 15360, 5120),  # skinny at the M boundary
+    (907, 2304, 768),    # narrow (160-wide) pair tiles, ragged last n-tile, two m-groups
+    (512, 5000, 4096),   # narrow, N not a multiple of 160
+    (907, 768, 768),     # BN=128 with a 4-CTA cluster (predictor O-proj)
+    (907, 768, 3072),    # same, FC2
 ])
 def test_gemm_matches_fp32(M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
