@@ -58,7 +58,6 @@ constexpr int kBarBytes = 256;
 constexpr int kSmem = 2 * kQTile + kRing * kEntry + kBarBytes + 1024;
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
-constexpr int kPolyEvery = 4;             // 1 in 4 key pairs exponentiated on the FMA pipe
 constexpr int kPartStride = kD + 4;       // partial row: O[128], m, l (16-byte aligned rows)
 constexpr int kMinBlocksPerCta = 3;
 }  // namespace
@@ -161,6 +160,7 @@ __device__ __forceinline__ UnitView unit_view(const FaParams& p, int u) {
   return v;
 }
 
+template <int POLY, bool LD_BATCH, int EXP = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     chunk_attn_fa_kernel(const __grid_constant__ CUtensorMap tmap_q,
                          const __grid_constant__ CUtensorMap tmap_kv, const FaParams p) {
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int pg_next = lane < 16 ? page_of(v.kb0) : 0;
       for (int j = 0; j < v.nblk; ++j) {
         const int pg = pg_next;
-        if (lane < 16 && j + 1 < v.nblk) pg_next = page_of(v.kb0 + j + 1);
+        if (lane < 16 && j + 1 < v.nblk) pg_next = page_of(EXP == 2 ? v.kb0 : v.kb0 + j + 1);
 #pragma unroll
         for (int kv = 0; kv < 2; ++kv, ++ent) {
           const int st = ent % kRing;
@@ -358,14 +358,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&s_full[t], s_cnt & 1);
         ++s_cnt;
         tc_fence_after();
+        if constexpr (EXP == 1) {  // timing experiment: no softmax work at all
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[t]);
+          continue;
+        }
         float s[kKeys];
+        if constexpr (LD_BATCH) {
+          uint32_t w[kKeys];
 #pragma unroll
-        for (int c = 0; c < kKeys / 32; ++c) {
-          uint32_t w[32];
-          tmem_ld_32x32b_x32(t_s + c * 32, w);
+          for (int c = 0; c < kKeys / 32; ++c)
+            tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(w + c * 32));
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(w[e]);
+          for (int e = 0; e < kKeys; ++e) s[e] = __uint_as_float(w[e]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < kKeys / 32; ++c) {
+            uint32_t w[32];
+            tmem_ld_32x32b_x32(t_s + c * 32, w);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(w[e]);
+          }
         }
         const int k0 = (v.kb0 + j) * kKeys;
         // blocks entirely below every row's diagonal need no mask (warp-uniform)
@@ -415,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int k = c * 32 + 2 * i;
             float x0, x1, e0, e1;
             f2_split(f2_fma(f2(s[k], s[k + 1]), sc2, nb2), x0, x1);
-            if ((i % kPolyEvery) == kPolyEvery - 1) {
+            if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == POLY - 1) {
               exp2_poly2(x0, x1, e0, e1);
             } else {
               e0 = ex2(x0);
@@ -625,10 +641,20 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   const uint64_t blocks = static_cast<uint64_t>(pool_pages) * g.n_layers * g.n_heads * 2;
   rc = make_tmap_kmajor(&tkv, pool, blocks * g.page_tokens, kD, g.page_tokens);
   if (rc) return rc;
+  // TK_FA_VARIANT (experiments): 0 poly 1/4 (default), 1 MUFU only, 2 poly 1/2,
+  // 3 poly 1/4 with one wait for the four S loads, 4 MUFU only + batched loads
+  static const int variant = getenv("TK_FA_VARIANT") ? atoi(getenv("TK_FA_VARIANT")) : 0;
+  using KernFn = void (*)(CUtensorMap, CUtensorMap, FaParams);
+  KernFn kern = variant == 1 ? (KernFn)chunk_attn_fa_kernel<0, false>
+              : variant == 2 ? (KernFn)chunk_attn_fa_kernel<2, false>
+              : variant == 3 ? (KernFn)chunk_attn_fa_kernel<4, true>
+              : variant == 4 ? (KernFn)chunk_attn_fa_kernel<0, true>
+              : variant == 5 ? (KernFn)chunk_attn_fa_kernel<4, false, 1>
+              : variant == 6 ? (KernFn)chunk_attn_fa_kernel<4, false, 2>
+                             : (KernFn)chunk_attn_fa_kernel<4, false>;
   static bool cfg = false;
   if (!cfg) {
-    TK_CUDA(cudaFuncSetAttribute(chunk_attn_fa_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     cfg = true;
   }
   FaParams prm;
@@ -643,7 +669,7 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   prm.n_heads = g.n_heads;
   prm.layer = layer;
   prm.scale_log2 = scale * 1.4426950408889634f;
-  chunk_attn_fa_kernel<<<plan.n_ctas, kThreads, kSmem, s>>>(tq, tkv, prm);
+  kern<<<plan.n_ctas, kThreads, kSmem, s>>>(tq, tkv, prm);
   TK_CUDA(cudaGetLastError());
   note_launch();
   if (plan.n_pieces > 0) {

@@ -654,10 +654,9 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
 // multicast to the CTAs of both pairs that hold that half, so weights are
 // still fetched once per GEMM.
 //
-// BN (tile width) is 256, or 160 for N=5120-class GEMMs (O-proj, FC2 at
-// M=512): 32 clusters of 512x160 cover N in exactly one wave, so no tile is
-// split and there is no stream-K fixup; 256-wide tiles would leave 40% of the
-// SMs idle or need a split-K exchange per tile.
+// BN (tile width) is 256 (stream-K), or 160 for a one-wave data-parallel
+// schedule: O-proj at M=512 as 32 clusters of 512x160 (no split tile); 256-
+// wide tiles would leave SMs idle or need a split-K exchange per tile.
 template <int BN>
 struct PairCfg {
   static constexpr int A_BYTES = 128 * 64 * 2;
@@ -975,7 +974,6 @@ int make_tmap_kv_pages(CUtensorMap* map, const void* pool, uint64_t blocks, uint
 }
 
 static int pick_bn(int N) { return N >= 1024 ? 256 : 128; }
-constexpr int kNarrowBN = 160;  // pair-kernel tile width for one-wave N=5120-class GEMMs
 
 // Co-resident clusters of size cs for the BN variant (queried once per variant).
 static int max_clusters_for(int bn, int cs);
@@ -1055,26 +1053,45 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
   pl.pair = pl.bn == 256 && pl.tiles_m % 2 == 0 && getenv("TK_NO_PAIR") == nullptr;
   pl.cs = pl.tiles_m % 4 == 0 ? 4 : (pl.tiles_m % 2 == 0 ? 2 : 1);
   if (pl.pair && pl.cs == 1) pl.cs = 2;
+  pl.kbs = K / 64;
   int clusters = pl.pair ? max_pair_clusters(pl.cs) : max_clusters_for(pl.bn, pl.cs);
   if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / pl.cs));
-  bool one_wave = false;
-  // (for long K the 256-wide stream-K schedule wins: narrow tiles re-read A
-  // from L2 for every 160 columns, and the fixup is amortised over many k-blocks)
-  if (pl.pair && K <= 8192 && getenv("TK_NO_NARROW") == nullptr) {
-    // narrow tiles when they cover the whole GEMM in one wave of clusters
-    const int groups_m = pl.tiles_m / pl.cs;
-    const int tn = (N + kNarrowBN - 1) / kNarrowBN;
-    if (tn * groups_m <= clusters && 4 * tn * groups_m >= 3 * clusters) {
-      pl.bn = kNarrowBN;
-      one_wave = true;
+  bool data_parallel = false;
+  if (pl.pair) {
+    // Tile shape.  Default: 256-wide tiles, stream-K over the clusters (every
+    // split tile costs a partial exchange).  When 160-wide tiles cover the
+    // GEMM in one wave of clusters and K is short (nothing to amortise the
+    // exchange over), a data-parallel schedule with one tile per cluster wins:
+    // O-proj at M=512 38 -> 46 us (measured); for long K (FC2) or several
+    // waves (QKV, FC1) the narrow tiles lose to their extra L2 traffic for A.
+    int fbn = 0, fcs = 0, fdp = -1;  // TK_GEMM_CFG="BN,CS,DP" forces a schedule (experiments)
+    if (const char* f = getenv("TK_GEMM_CFG")) sscanf(f, "%d,%d,%d", &fbn, &fcs, &fdp);
+    if (fdp >= 0 && (fbn == 256 || fbn == 160) && (fcs == 2 || (fcs == 4 && pl.tiles_m % 4 == 0))) {
+      pl.bn = fbn;
+      pl.cs = fcs;
+      clusters = max_pair_clusters(fcs);
+      if (max_ctas > 0) clusters = std::min(clusters, std::max(1, max_ctas / fcs));
+      if (fdp) {
+        const long long T = static_cast<long long>(pl.tiles_m / fcs) * ((N + fbn - 1) / fbn);
+        long long g = std::min<long long>(T, clusters);
+        while (T % g) --g;
+        clusters = static_cast<int>(g);
+        data_parallel = true;
+      }
+    } else if (K <= 8192 && getenv("TK_NO_NARROW") == nullptr) {
+      const int groups_m = pl.tiles_m / pl.cs;
+      const int tn = (N + 159) / 160;
+      if (tn * groups_m <= clusters && 4 * tn * groups_m >= 3 * clusters) {
+        pl.bn = 160;
+        clusters = tn * groups_m;  // one tile per cluster
+        data_parallel = true;
+      }
     }
   }
   pl.tiles_n = (N + pl.bn - 1) / pl.bn;
-  pl.kbs = K / 64;
   pl.total_iters = static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
-  if (one_wave) clusters = static_cast<int>(pl.total_iters / pl.kbs);  // one tile per cluster
   clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, pl.total_iters / 4)));
-  if (max_ctas <= 0 && !one_wave) clusters = pick_clusters(pl.total_iters, pl.kbs, clusters);
+  if (max_ctas <= 0 && !data_parallel) clusters = pick_clusters(pl.total_iters, pl.kbs, clusters);
   pl.clusters = clusters;
   // most CTAs (clusters) sharing one tile, over all cluster tiles
   const long long ctiles = pl.total_iters / pl.kbs;
@@ -1365,9 +1382,9 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
     CUtensorMap tb;
     rc = make_tmap_kmajor(&tb, B, N, K, pl.bn / 2 / (pl.cs / 2));
     if (rc) return rc;
-    if (pl.bn == kNarrowBN) {
-      if (pl.cs == 4) return pair_epi<4, kNarrowBN>(ta, tb, a, pl.clusters, stream);
-      return pair_epi<2, kNarrowBN>(ta, tb, a, pl.clusters, stream);
+    if (pl.bn == 160) {
+      if (pl.cs == 4) return pair_epi<4, 160>(ta, tb, a, pl.clusters, stream);
+      return pair_epi<2, 160>(ta, tb, a, pl.clusters, stream);
     }
     if (pl.cs == 4) return pair_epi<4, 256>(ta, tb, a, pl.clusters, stream);
     return pair_epi<2, 256>(ta, tb, a, pl.clusters, stream);

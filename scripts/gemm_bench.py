@@ -17,8 +17,9 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2401_11181_b200 import native  # noqa: E402
 
-SHAPES = {"qkv": (15360, 5120, native.EPI_BF16_BIAS), "o": (5120, 5120, native.EPI_F32_BIAS_RESID),
-          "fc1": (20480, 5120, native.EPI_BF16_BIAS_RELU), "fc2": (5120, 20480, native.EPI_F32_BIAS_RESID)}
+# epilogues as the runtime uses them (O-proj / FC2 store bf16; the next norm adds the residual)
+SHAPES = {"qkv": (15360, 5120, native.EPI_BF16_BIAS), "o": (5120, 5120, native.EPI_BF16_BIAS),
+          "fc1": (20480, 5120, native.EPI_BF16_BIAS_RELU), "fc2": (5120, 20480, native.EPI_BF16_BIAS)}
 
 
 def main():
@@ -27,6 +28,8 @@ def main():
     ap.add_argument("--m", type=int, nargs="*", default=[512])
     ap.add_argument("--shapes", nargs="*", default=list(SHAPES))
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--cublas", action="store_true",
+                    help="time torch.matmul (cuBLAS) on the same shapes instead, for reference")
     ap.add_argument("--epi", default=None, choices=["bf16", "f32", "resid"],
                     help="override the shape's epilogue (isolates epilogue cost)")
     args = ap.parse_args()
@@ -48,8 +51,13 @@ def main():
             nb = ctypes.c_int64()
             native.check(native.load().tk_gemm_workspace_bytes(M, N, K, ctypes.byref(nb)))
             ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")
+            if args.cublas:
+                bt = b.t()
+                run = lambda: torch.matmul(a, bt)  # noqa: E731
+            else:
+                run = lambda: native.gemm(a, b, bias=bias, epilogue=epi, out=out, workspace=ws)  # noqa: E731
             for _ in range(3):
-                native.gemm(a, b, bias=bias, epilogue=epi, out=out, workspace=ws)
+                run()
             torch.cuda.synchronize()
             times = []
             for _ in range(args.iters):
@@ -57,13 +65,13 @@ def main():
                     flush.zero_()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record()
-                native.gemm(a, b, bias=bias, epilogue=epi, out=out, workspace=ws)
+                run()
                 e.record()
                 e.synchronize()
                 times.append(s.elapsed_time(e))
             ms = sorted(times)[len(times) // 2]
             tf = 2 * M * N * K / (ms / 1e3) / 1e12
-            print(json.dumps({"shape": name, "epi": epi, "M": M, "N": N, "K": K, "median_us": round(ms * 1e3, 2),
+            print(json.dumps({"shape": name, "epi": "cublas" if args.cublas else epi, "M": M, "N": N, "K": K, "median_us": round(ms * 1e3, 2),
                               "tflops": round(tf, 1),
                               "frac_burst": round(tf / peak["bf16_tflops"], 3)}))
 
