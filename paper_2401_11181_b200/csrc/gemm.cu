@@ -63,6 +63,7 @@ struct GemmArgs {
   int epi;
   int tiles_m, tiles_n, kbs;
   long long total_iters;
+  QkvScatter kv;  // EPI_QKV_PAGED only
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -83,7 +84,8 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_store(const GemmArgs& p, int row, int col0,
                                                float (&v)[32]) {
   if (row >= p.M) return;
-  if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_RELU || EPI == EPI_F32_BIAS_RESID) {
+  if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_RELU || EPI == EPI_F32_BIAS_RESID ||
+                EPI == EPI_QKV_PAGED) {
     if (p.bias != nullptr) {
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -99,6 +101,27 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& p, int row, int c
   if constexpr (EPI == EPI_BF16_BIAS_RELU) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+  if constexpr (EPI == EPI_QKV_PAGED) {
+    const int hd = p.kv.g.n_heads * p.kv.g.head_dim;
+    if (col0 >= hd) {  // K or V: 32 columns of one head -> 64 contiguous bytes of a page slot
+      const TokenMeta m = p.kv.meta[row];
+      const int kv = col0 >= 2 * hd ? 1 : 0;
+      const int c = col0 - (1 + kv) * hd;
+      __nv_bfloat16* out = p.kv.pool +
+                           p.kv.g.offset(m.page, p.kv.layer, kv, c / p.kv.g.head_dim, m.slot) +
+                           c % p.kv.g.head_dim;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint4 o;
+        o.x = pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]);
+        o.y = pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]);
+        o.z = pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]);
+        o.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
+        *reinterpret_cast<uint4*>(out + g * 8) = o;
+      }
+      return;
+    }
   }
   if constexpr (EPI == EPI_F32_BIAS_RESID || EPI == EPI_F32) {
     float* out = reinterpret_cast<float*>(p.C) + static_cast<size_t>(row) * p.N + col0;
@@ -131,6 +154,64 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& p, int row, int c
         o.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
         *reinterpret_cast<uint4*>(out + g * 8) = o;
       }
+    }
+  }
+}
+
+// Stream-K partial tiles: [32-col chunk c][float4 group g][epilogue thread]
+// float4s, so each warp-wide store/load of one (c, g) moves 512 contiguous
+// bytes (the row-per-thread TMEM layout would otherwise touch 32 lines).
+__device__ __forceinline__ void partial_store(float* slot, int c, int tid, const uint32_t (&r)[32]) {
+  float4* dst = reinterpret_cast<float4*>(slot) + static_cast<size_t>(c) * 8 * 128 + tid;
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+    __stcg(dst + g * 128, make_float4(__uint_as_float(r[g * 4]), __uint_as_float(r[g * 4 + 1]),
+                                      __uint_as_float(r[g * 4 + 2]), __uint_as_float(r[g * 4 + 3])));
+}
+
+// Sum of the earlier contributors' partials for chunk c.
+__device__ __forceinline__ void partial_load(const float* tile_ws, size_t slot_elems, int n_slots,
+                                             int c, int tid, float4 (&out)[8]) {
+#pragma unroll
+  for (int g = 0; g < 8; ++g) out[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int a = 0; a < n_slots; ++a) {
+    const float4* src = reinterpret_cast<const float4*>(tile_ws + a * slot_elems) +
+                        static_cast<size_t>(c) * 8 * 128 + tid;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const float4 t = __ldcg(src + g * 128);
+      out[g].x += t.x; out[g].y += t.y; out[g].z += t.z; out[g].w += t.w;
+    }
+  }
+}
+
+// Last arriver of a split tile: TMEM accumulator + partials -> epilogue, the
+// partial loads of chunk c+1 in flight while chunk c is finished.
+template <int EPI, int NCHUNK>
+__device__ __forceinline__ void fixup_epilogue(const GemmArgs& p, uint32_t t_row, int row,
+                                               int col_base, const float* tile_ws,
+                                               size_t slot_elems, int n_slots, int tid) {
+  float4 cur[8];
+  partial_load(tile_ws, slot_elems, n_slots, 0, tid, cur);
+#pragma unroll 1
+  for (int c = 0; c < NCHUNK; ++c) {
+    float4 nxt[8];
+    if (c + 1 < NCHUNK) partial_load(tile_ws, slot_elems, n_slots, c + 1, tid, nxt);
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(t_row + c * 32, r);
+    tmem_wait_ld();
+    float v[32];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      v[g * 4] = __uint_as_float(r[g * 4]) + cur[g].x;
+      v[g * 4 + 1] = __uint_as_float(r[g * 4 + 1]) + cur[g].y;
+      v[g * 4 + 2] = __uint_as_float(r[g * 4 + 2]) + cur[g].z;
+      v[g * 4 + 3] = __uint_as_float(r[g * 4 + 3]) + cur[g].w;
+    }
+    epilogue_store<EPI>(p, row, col_base + c * 32, v);
+    if (c + 1 < NCHUNK) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g) cur[g] = nxt[g];
     }
   }
 }
@@ -315,11 +396,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
             uint32_t r[32];
             tmem_ld_32x32b_x32(t_row + c * 32, r);
             tmem_wait_ld();
-            float4* dst = reinterpret_cast<float4*>(mine + (static_cast<size_t>(c) * 128 + tid_e) * 32);
-#pragma unroll
-            for (int g = 0; g < 8; ++g)
-              __stcg(dst + g, make_float4(__uint_as_float(r[g * 4]), __uint_as_float(r[g * 4 + 1]),
-                                          __uint_as_float(r[g * 4 + 2]), __uint_as_float(r[g * 4 + 3])));
+            partial_store(mine, c, tid_e, r);
           }
           tc_fence_before();
           __syncwarp();
@@ -335,25 +412,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
           }
           named_bar_sync(1, 128);
           __threadfence();
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(t_row + c * 32, r);
-            tmem_wait_ld();
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            for (int a = 0; a < contrib - 1; ++a) {
-              const float4* src = reinterpret_cast<const float4*>(
-                  tile_ws + static_cast<size_t>(a) * slot_elems + (static_cast<size_t>(c) * 128 + tid_e) * 32);
-#pragma unroll
-              for (int g = 0; g < 8; ++g) {
-                const float4 t = __ldcg(src + g);
-                v[g * 4] += t.x; v[g * 4 + 1] += t.y; v[g * 4 + 2] += t.z; v[g * 4 + 3] += t.w;
-              }
-            }
-            epilogue_store<EPI>(p, row, col_base + c * 32, v);
-          }
+          fixup_epilogue<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems, contrib - 1,
+                                       tid_e);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -662,7 +722,7 @@ struct PairCfg {
   static constexpr int A_BYTES = 128 * 64 * 2;
   static constexpr int BH_BYTES = (BN / 2) * 64 * 2;
   static constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
-  static constexpr int STAGES = (220 * 1024 - 2048) / STAGE_BYTES > 8 ? 8 : (220 * 1024 - 2048) / STAGE_BYTES;
+  static constexpr int STAGES = (232448 - 2048) / STAGE_BYTES > 8 ? 8 : (232448 - 2048) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 256 + 1024;
 };
 
@@ -858,11 +918,7 @@ __global__ void __launch_bounds__(192, 1)
             uint32_t r[32];
             tmem_ld_32x32b_x32(t_row + c * 32, r);
             tmem_wait_ld();
-            float4* dst = reinterpret_cast<float4*>(mine + (static_cast<size_t>(c) * 128 + tid_e) * 32);
-#pragma unroll
-            for (int g = 0; g < 8; ++g)
-              __stcg(dst + g, make_float4(__uint_as_float(r[g * 4]), __uint_as_float(r[g * 4 + 1]),
-                                          __uint_as_float(r[g * 4 + 2]), __uint_as_float(r[g * 4 + 3])));
+            partial_store(mine, c, tid_e, r);
           }
           release_tmem();
           __threadfence();
@@ -876,25 +932,8 @@ __global__ void __launch_bounds__(192, 1)
           }
           named_bar_sync(1, 128);
           __threadfence();
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(t_row + c * 32, r);
-            tmem_wait_ld();
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            for (int a = 0; a < contrib - 1; ++a) {
-              const float4* src = reinterpret_cast<const float4*>(
-                  tile_ws + static_cast<size_t>(a) * slot_elems + (static_cast<size_t>(c) * 128 + tid_e) * 32);
-#pragma unroll
-              for (int g = 0; g < 8; ++g) {
-                const float4 t = __ldcg(src + g);
-                v[g * 4] += t.x; v[g * 4 + 1] += t.y; v[g * 4 + 2] += t.z; v[g * 4 + 3] += t.w;
-              }
-            }
-            epilogue_store<EPI>(p, row, col_base + c * 32, v);
-          }
+          fixup_epilogue<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems, contrib - 1,
+                                       tid_e);
           release_tmem();
           named_bar_sync(1, 128);
           if (ep_leader) {
@@ -1178,6 +1217,7 @@ static int pair_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs
     case EPI_BF16_BIAS_RELU: return launch_pair<EPI_BF16_BIAS_RELU, CS, BN>(ta, tb, a, clusters, s);
     case EPI_F32_BIAS_RESID: return launch_pair<EPI_F32_BIAS_RESID, CS, BN>(ta, tb, a, clusters, s);
     case EPI_F32: return launch_pair<EPI_F32, CS, BN>(ta, tb, a, clusters, s);
+    case EPI_QKV_PAGED: return launch_pair<EPI_QKV_PAGED, CS, BN>(ta, tb, a, clusters, s);
   }
   set_error("unknown gemm epilogue");
   return TK_EINVAL;
@@ -1301,6 +1341,7 @@ static int dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
     case EPI_BF16_BIAS_RELU: return launch_gemm<BN, EPI_BF16_BIAS_RELU, CS>(ta, tb, a, clusters, s);
     case EPI_F32_BIAS_RESID: return launch_gemm<BN, EPI_F32_BIAS_RESID, CS>(ta, tb, a, clusters, s);
     case EPI_F32: return launch_gemm<BN, EPI_F32, CS>(ta, tb, a, clusters, s);
+    case EPI_QKV_PAGED: return launch_gemm<BN, EPI_QKV_PAGED, CS>(ta, tb, a, clusters, s);
   }
   set_error("unknown gemm epilogue");
   return TK_EINVAL;
@@ -1319,8 +1360,15 @@ static int dispatch_cs(const void* B, int N, int K, const CUtensorMap& ta, GemmA
   }
 }
 
+bool gemm_is_skinny(int M) { return M <= kSkinnyMaxM && getenv("TK_NO_SKINNY") == nullptr; }
+
 int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, int N, int K,
-              int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas) {
+              int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas,
+              const QkvScatter* scatter) {
+  TK_CHECK(epi != EPI_QKV_PAGED || (scatter && !gemm_is_skinny(M) && N % 32 == 0 &&
+                                    N == 3 * scatter->g.n_heads * scatter->g.head_dim &&
+                                    scatter->g.head_dim % 32 == 0),
+           TK_EINVAL, "gemm: EPI_QKV_PAGED needs a scatter target, M above the skinny range");
   TK_CHECK(M > 0 && N > 0 && K > 0, TK_EINVAL, "gemm: empty problem");
   TK_CHECK(K % 64 == 0, TK_EINVAL, "gemm: K must be a multiple of 64");
   TK_CHECK(N % 8 == 0, TK_EINVAL, "gemm: N must be a multiple of 8");
@@ -1377,6 +1425,7 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   (void)tiles;
   a.counters = static_cast<int*>(workspace);
   a.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
+  a.kv = scatter ? *scatter : QkvScatter{};
   if (pl.pair) {
     // each CTA loads 64-row (CS=4) or 128-row (CS=2) slices of its B half
     CUtensorMap tb;

@@ -414,16 +414,23 @@ static int run_layer(tk_instance* inst, int layer, int n, const TokenMeta* meta_
                            hi, m.norm_eps, !opt, s);
   });
   if (rc) return rc;
+  // OPT (no rotary embedding) above the skinny range: the QKV epilogue writes
+  // K/V straight into the pages; otherwise a kv_write pass (RoPE for Llama).
+  const bool fused_kv = opt && !gemm_is_skinny(n);
+  const QkvScatter scatter{meta_dev, inst->pool, inst->geom, layer};
   rc = profiled(inst, s, PK_QKV, 2 * nn * 3 * h * h, (3 * h * h + nn * 4 * h) * 2, [&] {
     return gemm_bf16(inst->xn, L.qkv_w, inst->qkv, L.qkv_b, n, 3 * hi, hi,
-                     opt ? EPI_BF16_BIAS : EPI_BF16, inst->gemm_ws, inst->gemm_ws_bytes, s);
+                     fused_kv ? EPI_QKV_PAGED : (opt ? EPI_BF16_BIAS : EPI_BF16), inst->gemm_ws,
+                     inst->gemm_ws_bytes, s, 0, fused_kv ? &scatter : nullptr);
   });
   if (rc) return rc;
-  rc = profiled(inst, s, PK_OTHER, 0, nn * h * 8, [&] {
-    return launch_kv_write(inst->qkv, meta_dev, n, inst->pool, inst->geom, layer, 1.f,
-                           opt ? 0 : 1, m.rope_theta, s);
-  });
-  if (rc) return rc;
+  if (!fused_kv) {
+    rc = profiled(inst, s, PK_OTHER, 0, nn * h * 8, [&] {
+      return launch_kv_write(inst->qkv, meta_dev, n, inst->pool, inst->geom, layer, 1.f,
+                             opt ? 0 : 1, m.rope_theta, s);
+    });
+    if (rc) return rc;
+  }
   rc = profiled(inst, s, PK_ATTN, attn_flops, attn_bytes, attention_fn);
   if (rc) return rc;
   rc = profiled(inst, s, PK_O, 2 * nn * h * h, (h * h + nn * h) * 2 + nn * h * 2, [&] {

@@ -19,11 +19,8 @@ enum Epi : int {
   EPI_BF16_BIAS_RELU = 2,  // C bf16 = relu(acc + bias)
   EPI_F32_BIAS_RESID = 3,  // C fp32 += acc + bias (residual stream, in place)
   EPI_F32 = 4,             // C fp32 = acc (logits)
+  EPI_QKV_PAGED = 5,       // fused QKV (+bias): Q columns -> C bf16, K/V columns -> KV pages
 };
-
-int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, int N, int K,
-              int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas = 0);
-int64_t gemm_workspace_bytes(int M, int N, int K);
 
 // Page-major KV pool geometry: [page][layer][head][K|V][page_tokens][head_dim] bf16.
 // K and V of one (page, layer, head) are adjacent 4 KB blocks (head_dim 128),
@@ -49,6 +46,24 @@ struct TokenMeta {
   int32_t slot;
   int32_t slice;
 };
+
+// EPI_QKV_PAGED target: token rows' K/V go straight from the GEMM epilogue to
+// their pages (the separate kv_write pass and its 2x10 MB of traffic per
+// OPT-13B chunk layer disappear).  No rotary embedding (OPT).
+struct QkvScatter {
+  const TokenMeta* meta;
+  __nv_bfloat16* pool;
+  KvGeom g;
+  int layer;
+};
+
+int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, int N, int K,
+              int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas = 0,
+              const QkvScatter* scatter = nullptr);
+int64_t gemm_workspace_bytes(int M, int N, int K);
+// true when gemm_bf16 takes the swap-AB weight-streaming path for this M
+// (that path has no EPI_QKV_PAGED epilogue)
+bool gemm_is_skinny(int M);
 
 int launch_embed_opt(const int32_t* ids, const TokenMeta* meta, int n, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* pos_emb, float* resid, int hidden, cudaStream_t s);
