@@ -504,43 +504,58 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Merge the pieces of every split (pair, head): one warp per query row, each
-// lane 4 of the 128 dims; partials are read coalesced (512 B per piece-row).
+// lane 4 of the 128 dims; up to 4 pieces are loaded at once (one round trip
+// for the usual 2-3), partial rows read coalesced (512 B per piece-row).
 __global__ void __launch_bounds__(256)
     fa_combine_kernel(__nv_bfloat16* __restrict__ o, const FaPair* __restrict__ pairs,
                       const FaGroup* __restrict__ groups, int n_heads,
                       const float* __restrict__ partial) {
-  const int pair = blockIdx.x >> 5, t = (blockIdx.x >> 4) & 1, rg = blockIdx.x & 15;
-  const int head = blockIdx.y;
-  const FaGroup g = groups[pair * n_heads + head];
-  if (g.n_pieces <= 1) return;
-  const FaPair pr = pairs[pair];
+  const FaGroup g = groups[blockIdx.x >> 5];
+  const int t = (blockIdx.x >> 4) & 1, rg = blockIdx.x & 15;
+  const FaPair pr = pairs[g.pair];
   const int nrows = t ? pr.nrows1 : pr.nrows0;
   const int r = rg * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= nrows) return;
   auto row_of = [&](int x) {
     return partial + ((static_cast<size_t>(g.first_piece + x) * 2 + t) * kRows + r) * kPartStride;
   };
-  float M = -INFINITY;
-  for (int x = 0; x < g.n_pieces; ++x) M = fmaxf(M, __ldcg(row_of(x) + kD));
-  float L = 0.f;
+  float M = -INFINITY, L = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int x = 0; x < g.n_pieces; ++x) {
-    const float* src = row_of(x);
-    const float m = __ldcg(src + kD);
-    const float w = (m == -INFINITY) ? 0.f : exp2f(m - M);
-    L += w * __ldcg(src + kD + 1);
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(src) + lane);
-    acc.x += w * v.x;
-    acc.y += w * v.y;
-    acc.z += w * v.z;
-    acc.w += w * v.w;
+  for (int base = 0; base < g.n_pieces; base += 4) {
+    float m[4], l[4];
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (base + k < g.n_pieces) {
+        const float* src = row_of(base + k);
+        m[k] = __ldcg(src + kD);
+        l[k] = __ldcg(src + kD + 1);
+        v[k] = __ldcg(reinterpret_cast<const float4*>(src) + lane);
+      } else {
+        m[k] = -INFINITY;
+        l[k] = 0.f;
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    const float Mn = fmaxf(fmaxf(M, fmaxf(m[0], m[1])), fmaxf(m[2], m[3]));
+    if (Mn == -INFINITY) continue;
+    const float c = (M == -INFINITY) ? 0.f : exp2f(M - Mn);
+    L *= c;
+    acc.x *= c; acc.y *= c; acc.z *= c; acc.w *= c;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float w = (m[k] == -INFINITY) ? 0.f : exp2f(m[k] - Mn);
+      L += w * l[k];
+      acc.x += w * v[k].x; acc.y += w * v[k].y; acc.z += w * v[k].z; acc.w += w * v[k].w;
+    }
+    M = Mn;
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
   uint2 pk;
   pk.x = pack_bf16x2(acc.x * inv, acc.y * inv);
   pk.y = pack_bf16x2(acc.z * inv, acc.w * inv);
   *reinterpret_cast<uint2*>(o + static_cast<size_t>(pr.row0 + t * kRows + r) * n_heads * kD +
-                            head * kD + lane * 4) = pk;
+                            g.head * kD + lane * 4) = pk;
 }
 
 // ------------------------------------------------------------------ host side
@@ -569,12 +584,11 @@ int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_cta
     }
     row += sl.len;
   }
-  if (np * n_heads > gcap) return -1;
   const long long T = per_head * n_heads;
   int G = static_cast<int>(std::min<long long>(std::max(1, max_ctas),
                                                std::max<long long>(1, T / kMinBlocksPerCta)));
   if (G + 1 > ocap) return -1;
-  int nu = 0, piece = 0;
+  int nu = 0, piece = 0, n_groups = 0;
   long long cur = 0;
   for (int h = 0; h < n_heads; ++h) {
     for (int q = 0; q < np; ++q) {
@@ -590,12 +604,9 @@ int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_cta
         s += take;
         cur += take;
       }
-      FaGroup& g = groups[q * n_heads + h];
-      g.n_pieces = nu - first;
-      g.first_piece = -1;
-      if (g.n_pieces > 1) {
-        if (piece + g.n_pieces > kFaMaxPieces) return -1;
-        g.first_piece = piece;
+      if (nu - first > 1) {
+        if (piece + (nu - first) > kFaMaxPieces || n_groups >= gcap) return -1;
+        groups[n_groups++] = FaGroup{piece, nu - first, q, h};
         for (int k = first; k < nu; ++k) units[k].piece = piece++;
       }
     }
@@ -619,6 +630,7 @@ int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_cta
   plan->n_units = nu;
   plan->n_ctas = G;
   plan->n_pieces = piece;
+  plan->n_groups = n_groups;
   return 0;
 }
 
@@ -672,9 +684,9 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   kern<<<plan.n_ctas, kThreads, kSmem, s>>>(tq, tkv, prm);
   TK_CUDA(cudaGetLastError());
   note_launch();
-  if (plan.n_pieces > 0) {
-    fa_combine_kernel<<<dim3(plan.n_pairs * 32, g.n_heads), 256, 0, s>>>(o, pairs_dev, groups_dev,
-                                                                       g.n_heads, partial);
+  if (plan.n_groups > 0) {
+    fa_combine_kernel<<<plan.n_groups * 32, 256, 0, s>>>(o, pairs_dev, groups_dev, g.n_heads,
+                                                         partial);
     TK_CUDA(cudaGetLastError());
     note_launch();
   }

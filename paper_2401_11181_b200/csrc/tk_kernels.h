@@ -116,11 +116,11 @@ struct FaUnit {
   int32_t pair, head, kb0, kb1;        // key blocks [kb0, kb1) of this (pair, head)
   int32_t piece;                       // partial slot (-1: the whole (pair, head), written directly)
 };
-struct FaGroup {
-  int32_t first_piece, n_pieces;       // pieces of one (pair, head)
+struct FaGroup {                       // a (pair, head) computed as several pieces
+  int32_t first_piece, n_pieces, pair, head;
 };
 struct FaPlan {
-  int n_pairs, n_units, n_ctas, n_pieces;
+  int n_pairs, n_units, n_ctas, n_pieces, n_groups;
 };
 // Host-side plan; arrays are caller-provided with capacities.  0 / -1 (overflow).
 int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_ctas, FaPlan* plan,
