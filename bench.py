@@ -143,6 +143,24 @@ def measured_peaks() -> dict:
             "source": "fallback (B200_PROFILING.md)"}
 
 
+def gemm_traffic(prof: dict):
+    """DRAM bytes per GEMM launch (dram__bytes_read.sum + dram__bytes_write.sum from the
+    committed ncu --set full captures, profiles/r01_gemm_traffic.json), weighted by this
+    run's launches of each shape, next to the algorithmic bytes of the same launches."""
+    p = ROOT / "profiles" / "r01_gemm_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    kinds = {"qkv_gemm": "qkv", "o_gemm": "o", "fc1_gemm": "fc1", "fc2_gemm": "fc2"}
+    n = sum(prof[k]["launches"] for k in kinds)
+    if not n:
+        return None
+    dram = sum(prof[k]["launches"] * d["dram_bytes_per_launch"][v] for k, v in kinds.items()) / n
+    alg = sum(prof[k]["launches"] * d["algorithmic_bytes_per_launch"][v] for k, v in kinds.items()) / n
+    return {"dram_bytes_per_launch": int(dram), "algorithmic_bytes_per_launch": int(alg),
+            "ratio": round(dram / alg, 3), "source": "profiles/r01_gemm_traffic.json (M=512 shapes)"}
+
+
 # ---------------------------------------------------------------- CPU port (oracle)
 
 def cpu_port_sample(plan_chunks, max_seconds: float = 25.0, threads: int | None = None):
@@ -343,6 +361,7 @@ def run_ours(args, world, rank, local):
     g_fl = sum(prof[k]["flops"] for k in gemm_kinds)
     g_n = sum(prof[k]["launches"] for k in gemm_kinds)
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms else 0.0
+    traffic = gemm_traffic(prof)
     peak = peaks["bf16_tflops_sustained"]
     attn = prof["attention"]
     if rank != 0:
@@ -380,7 +399,8 @@ def run_ours(args, world, rank, local):
             "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
             "peak_source": peaks["source"] + " bf16_tflops_sustained",
             "launches": g_n, "avg_launch_us": round(g_ms * 1e3 / max(1, g_n), 2),
-            "traffic": None,
+            "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+            "traffic_detail": traffic,
         },
         "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                         "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 2) if v["ms"] and v["flops"] else None,
