@@ -164,6 +164,7 @@ template <int POLY, bool LD_BATCH, int EXP = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     chunk_attn_fa_kernel(const __grid_constant__ CUtensorMap tmap_q,
                          const __grid_constant__ CUtensorMap tmap_kv, const FaParams p) {
+  griddep_launch();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -510,6 +511,7 @@ __global__ void __launch_bounds__(256)
     fa_combine_kernel(__nv_bfloat16* __restrict__ o, const FaPair* __restrict__ pairs,
                       const FaGroup* __restrict__ groups, int n_heads,
                       const float* __restrict__ partial) {
+  griddep_launch();
   const FaGroup g = groups[blockIdx.x >> 5];
   const int t = (blockIdx.x >> 4) & 1, rg = blockIdx.x & 15;
   const FaPair pr = pairs[g.pair];

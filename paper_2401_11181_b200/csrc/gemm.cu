@@ -268,39 +268,55 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
   constexpr int B_SLICE_ROWS = BN / CS;
   constexpr int B_SLICE_BYTES = B_SLICE_ROWS * Cfg::BK * 2;
 
+  // programmatic dependent launch: everything but the producer's first weight
+  // tiles waits for the previous kernel on the stream
+  griddep_launch();
+  if (warp != 0) griddep_wait();
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       const uint64_t pol_a = l2_policy_evict_last();   // activations: reused by every n-tile
       const uint64_t pol_b = l2_policy_evict_first();  // weights: streamed once per GEMM
-      int stage = 0;
-      uint32_t phase = 0;
-      for (long long i = it_begin; i < it_end;) {
-        const int ctile = static_cast<int>(i / kbs);
-        const long long seg_end = min(it_end, static_cast<long long>(ctile + 1) * kbs);
+      auto load_a = [&](long long i, int stage) {
+        const int ctile = static_cast<int>(i / kbs), kb = static_cast<int>(i % kbs);
         const int m_idx = (ctile % groups_m) * CS + rank;
+        tma_load_2d(sa + stage * Cfg::A_BYTES, &tmap_a, &full[stage], kb * Cfg::BK,
+                    m_idx * Cfg::BM, pol_a);
+      };
+      auto load_b = [&](long long i, int stage) {
+        const int ctile = static_cast<int>(i / kbs), kb = static_cast<int>(i % kbs);
         const int n_idx = ctile / groups_m;
-        for (int kb = static_cast<int>(i - static_cast<long long>(ctile) * kbs);
-             kb < static_cast<int>(seg_end - static_cast<long long>(ctile) * kbs); ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sa + stage * Cfg::A_BYTES, &tmap_a, &full[stage], kb * Cfg::BK,
-                      m_idx * Cfg::BM, pol_a);
-          if constexpr (CS == 1) {
-            tma_load_2d(sb + stage * Cfg::B_BYTES, &tmap_b, &full[stage], kb * Cfg::BK,
-                        n_idx * BN, pol_b);
-          } else {
-            tma_load_2d_mc(sb + stage * Cfg::B_BYTES + rank * B_SLICE_BYTES, &tmap_b,
-                           &full[stage], kb * Cfg::BK, n_idx * BN + rank * B_SLICE_ROWS, kMask,
-                           pol_b);
-          }
-          if (++stage == Cfg::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        if constexpr (CS == 1) {
+          tma_load_2d(sb + stage * Cfg::B_BYTES, &tmap_b, &full[stage], kb * Cfg::BK, n_idx * BN,
+                      pol_b);
+        } else {
+          tma_load_2d_mc(sb + stage * Cfg::B_BYTES + rank * B_SLICE_BYTES, &tmap_b, &full[stage],
+                         kb * Cfg::BK, n_idx * BN + rank * B_SLICE_ROWS, kMask, pol_b);
         }
-        i = seg_end;
+      };
+      // Weight tiles of the first stages do not depend on the previous kernel:
+      // issue them before the programmatic-launch dependency wait.
+      const int pre = static_cast<int>(min<long long>(it_end - it_begin, Cfg::STAGES));
+      for (int st = 0; st < pre; ++st) {
+        mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
+        load_b(it_begin + st, st);
       }
+      griddep_wait();
+      for (int st = 0; st < pre; ++st) load_a(it_begin + st, st);
+      int stage = pre % Cfg::STAGES;
+      uint32_t phase = pre == Cfg::STAGES ? 1u : 0u;
+      for (long long i = it_begin + pre; i < it_end; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+        load_a(i, stage);
+        load_b(i, stage);
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    } else {
+      griddep_wait();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -533,29 +549,45 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
   const long long it_end = static_cast<long long>(blockIdx.x + 1) * T / G;
   const int kbs = p.kbs;
 
+  // programmatic dependent launch: everything but the producer's first weight
+  // tiles waits for the previous kernel on the stream
+  griddep_launch();
+  if (warp != 0) griddep_wait();
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_w = l2_policy_evict_first();
       const uint64_t pol_x = l2_policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (long long i = it_begin; i < it_end;) {
-        const int tile = static_cast<int>(i / kbs);
-        const long long seg_end = min(it_end, static_cast<long long>(tile + 1) * kbs);
-        for (int kb = static_cast<int>(i - static_cast<long long>(tile) * kbs);
-             kb < static_cast<int>(seg_end - static_cast<long long>(tile) * kbs); ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sw + stage * Cfg::W_BYTES, &tmap_w, &full[stage], kb * Cfg::BK,
-                      tile * Cfg::BM, pol_w);
-          tma_load_2d(sx + stage * Cfg::X_BYTES, &tmap_x, &full[stage], kb * Cfg::BK, 0, pol_x);
-          if (++stage == Cfg::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        i = seg_end;
+      auto load_w = [&](long long i, int stage) {
+        tma_load_2d(sw + stage * Cfg::W_BYTES, &tmap_w, &full[stage],
+                    static_cast<int>(i % kbs) * Cfg::BK, static_cast<int>(i / kbs) * Cfg::BM, pol_w);
+      };
+      auto load_x = [&](long long i, int stage) {
+        tma_load_2d(sx + stage * Cfg::X_BYTES, &tmap_x, &full[stage],
+                    static_cast<int>(i % kbs) * Cfg::BK, 0, pol_x);
+      };
+      // the weight stream starts before the dependency wait (decode: the
+      // previous kernel's tail overlaps this kernel's first weight tiles)
+      const int pre = static_cast<int>(min<long long>(it_end - it_begin, Cfg::STAGES));
+      for (int st = 0; st < pre; ++st) {
+        mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
+        load_w(it_begin + st, st);
       }
+      griddep_wait();
+      for (int st = 0; st < pre; ++st) load_x(it_begin + st, st);
+      int stage = pre % Cfg::STAGES;
+      uint32_t phase = pre == Cfg::STAGES ? 1u : 0u;
+      for (long long i = it_begin + pre; i < it_end; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+        load_w(i, stage);
+        load_x(i, stage);
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    } else {
+      griddep_wait();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -790,36 +822,51 @@ __global__ void __launch_bounds__(192, 1)
   const uint16_t half_mask = static_cast<uint16_t>(CS == 4 ? ((1u << half) | (1u << (half + 2)))
                                                            : (1u << half));
 
+  // programmatic dependent launch: everything but the producer's first weight
+  // tiles waits for the previous kernel on the stream
+  griddep_launch();
+  if (warp != 0) griddep_wait();
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_a = l2_policy_evict_last();
       const uint64_t pol_b = l2_policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (long long i = it_begin; i < it_end;) {
-        const int ctile = static_cast<int>(i / kbs);
-        const long long seg_end = min(it_end, static_cast<long long>(ctile + 1) * kbs);
+      auto load_a = [&](long long i, int stage) {
+        const int ctile = static_cast<int>(i / kbs), kb = static_cast<int>(i % kbs);
         const int m_idx = (ctile % groups_m) * CS + rank;  // this CTA's 128-row tile
+        tma_load_2d_pair(sa + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, m_idx * BM, pol_a);
+      };
+      auto load_b = [&](long long i, int stage) {
+        const int ctile = static_cast<int>(i / kbs), kb = static_cast<int>(i % kbs);
         const int n_idx = ctile / groups_m;
-        for (int kb = static_cast<int>(i - static_cast<long long>(ctile) * kbs);
-             kb < static_cast<int>(seg_end - static_cast<long long>(ctile) * kbs); ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_expect_tx(&full[stage], PAIR_STAGE_BYTES);
-          tma_load_2d_pair(sa + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, m_idx * BM,
-                           pol_a);
-          const int brow = n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS;
-          uint8_t* bdst = sb + stage * BH_BYTES + pair * SLICE_BYTES;
-          if constexpr (CS == 2)
-            tma_load_2d_pair(bdst, &tmap_b, &full[stage], kb * BK, brow, pol_b);
-          else
-            tma_load_2d_pair_mc(bdst, &tmap_b, &full[stage], kb * BK, brow, half_mask, pol_b);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        i = seg_end;
+        const int brow = n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS;
+        uint8_t* bdst = sb + stage * BH_BYTES + pair * SLICE_BYTES;
+        if constexpr (CS == 2)
+          tma_load_2d_pair(bdst, &tmap_b, &full[stage], kb * BK, brow, pol_b);
+        else
+          tma_load_2d_pair_mc(bdst, &tmap_b, &full[stage], kb * BK, brow, half_mask, pol_b);
+      };
+      // weight tiles first (independent of the previous kernel), then wait for it
+      const int pre = static_cast<int>(min<long long>(it_end - it_begin, STAGES));
+      for (int st = 0; st < pre; ++st) {
+        if (leader) mbar_expect_tx(&full[st], PAIR_STAGE_BYTES);
+        load_b(it_begin + st, st);
       }
+      griddep_wait();
+      for (int st = 0; st < pre; ++st) load_a(it_begin + st, st);
+      int stage = pre % STAGES;
+      uint32_t phase = pre == STAGES ? 1u : 0u;
+      for (long long i = it_begin + pre; i < it_end; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (leader) mbar_expect_tx(&full[stage], PAIR_STAGE_BYTES);
+        load_a(i, stage);
+        load_b(i, stage);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    } else {
+      griddep_wait();
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
@@ -1150,6 +1197,17 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
 
 int64_t gemm_workspace_bytes(int M, int N, int K) { return plan_gemm(M, N, K, 0).ws_bytes; }
 
+// Programmatic dependent launch (TK_NO_PDL=1 disables): the GEMM may start
+// while the previous kernel on the stream drains; its producer prefetches
+// weight tiles and then waits (griddepcontrol.wait) before touching activations.
+static int set_pdl(cudaLaunchAttribute* attr, int n) {
+  static const bool off = getenv("TK_NO_PDL") != nullptr;
+  if (off) return n;
+  attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n].val.programmaticStreamSerializationAllowed = 1;
+  return n + 1;
+}
+
 template <int NB, int EPI>
 static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& a,
                          int ctas, cudaStream_t stream) {
@@ -1161,7 +1219,15 @@ static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const Gem
                                  Cfg::SMEM_BYTES));
     configured = true;
   }
-  kern<<<ctas, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tw, tx, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  cfg.numAttrs = set_pdl(attr, 0);
+  cfg.attrs = attr;
+  TK_CUDA(cudaLaunchKernelEx(&cfg, kern, tw, tx, a));
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;
@@ -1196,13 +1262,13 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = PairCfg<BN>::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = set_pdl(attr, 1);
   TK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
   note_launch();
   return TK_OK;
@@ -1281,13 +1347,13 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = set_pdl(attr, 1);
   TK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
   note_launch();
   return TK_OK;

@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kNormThreads)
                 const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ b,
                 __nv_bfloat16* __restrict__ y, int cols, float eps) {
   __shared__ float red[kNormThreads / 32];
+  griddep_launch();  // the GEMM that consumes y may start prefetching its weights
   float* xr = x + static_cast<size_t>(blockIdx.x) * cols;
   __nv_bfloat16* yr = y + static_cast<size_t>(blockIdx.x) * cols;
   float v[kNormMaxPer];
@@ -792,6 +793,7 @@ template <int D>
 __global__ void decode_combine_kernel(__nv_bfloat16* __restrict__ o, int n_heads,
                                       const int32_t* __restrict__ ctx_lens,
                                       const float* __restrict__ ws, int max_splits) {
+  griddep_launch();
   const int head = blockIdx.x, b = blockIdx.y;
   const int n_splits = (ctx_lens[b] + kDecSplitTokens - 1) / kDecSplitTokens;
   if (n_splits <= 1) return;

@@ -199,6 +199,16 @@ __device__ __forceinline__ void cluster_sync_all() {
                    : "memory");
 }
 
+// Programmatic dependent launch: block until the preceding kernel on the
+// stream has completed and its writes are visible (no-op without PDL).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next (PDL-launched) kernel on the stream be scheduled now: it only
+// prefetches weights until its griddep_wait().  Used in kernels whose whole
+// grid is resident at once, so early dependents cannot starve them.
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }

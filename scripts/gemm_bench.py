@@ -32,8 +32,12 @@ def main():
                     help="time torch.matmul (cuBLAS) on the same shapes instead, for reference")
     ap.add_argument("--epi", default=None, choices=["bf16", "f32", "resid"],
                     help="override the shape's epilogue (isolates epilogue cost)")
+    ap.add_argument("--chain", type=int, default=0,
+                    help="time N back-to-back layers of all --shapes (decode-style weight streaming)")
     args = ap.parse_args()
     native.load()
+    if args.chain:
+        return chain(args)
     peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for M in args.m:
@@ -74,6 +78,48 @@ def main():
             print(json.dumps({"shape": name, "epi": "cublas" if args.cublas else epi, "M": M, "N": N, "K": K, "median_us": round(ms * 1e3, 2),
                               "tflops": round(tf, 1),
                               "frac_burst": round(tf / peak["bf16_tflops"], 3)}))
+
+
+def chain(args):
+    """--chain N: N layers x (the shapes in order) back to back, no L2 flush; weights are
+    distinct per layer (larger than L2), like a decode step's GEMM sequence."""
+    import ctypes
+    for M in args.m:
+        layers = []
+        for li in range(args.chain):
+            ops = []
+            for name in args.shapes:
+                N, K, epi = SHAPES[name]
+                b = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+                ops.append((N, K, epi, b))
+            layers.append(ops)
+        acts = {K: torch.randn(M, K, device="cuda").bfloat16() for K in {5120, 20480}}
+        outs = {}
+        nb = ctypes.c_int64()
+        ws_bytes = 0
+        for N, K, epi, _ in layers[0]:
+            native.check(native.load().tk_gemm_workspace_bytes(M, N, K, ctypes.byref(nb)))
+            ws_bytes = max(ws_bytes, nb.value)
+            outs[(N, K)] = torch.zeros(M, N, device="cuda",
+                                       dtype=torch.float32 if epi >= 3 else torch.bfloat16)
+        ws = torch.zeros(ws_bytes, dtype=torch.uint8, device="cuda")
+
+        def run():
+            for ops in layers:
+                for N, K, epi, b in ops:
+                    native.gemm(acts[K], b, epilogue=epi, out=outs[(N, K)], workspace=ws)
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        run()
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e)
+        wbytes = sum(N * K * 2 for ops in layers for N, K, _, _ in ops)
+        print(json.dumps({"chain_layers": args.chain, "M": M, "shapes": args.shapes,
+                          "ms": round(ms, 3), "weight_gbs": round(wbytes / ms / 1e6, 1)}))
 
 
 if __name__ == "__main__":
