@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
       };
       // Weight tiles of the first stages do not depend on the previous kernel:
       // issue them before the programmatic-launch dependency wait.
-      const int pre = static_cast<int>(min<long long>(it_end - it_begin, Cfg::STAGES));
+      const int pre = static_cast<int>(it_end - it_begin < Cfg::STAGES ? it_end - it_begin : Cfg::STAGES);
       for (int st = 0; st < pre; ++st) {
         mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
         load_b(it_begin + st, st);
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
       };
       // the weight stream starts before the dependency wait (decode: the
       // previous kernel's tail overlaps this kernel's first weight tiles)
-      const int pre = static_cast<int>(min<long long>(it_end - it_begin, Cfg::STAGES));
+      const int pre = static_cast<int>(it_end - it_begin < Cfg::STAGES ? it_end - it_begin : Cfg::STAGES);
       for (int st = 0; st < pre; ++st) {
         mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
         load_w(it_begin + st, st);
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_2d_pair_mc(bdst, &tmap_b, &full[stage], kb * BK, brow, half_mask, pol_b);
       };
       // weight tiles first (independent of the previous kernel), then wait for it
-      const int pre = static_cast<int>(min<long long>(it_end - it_begin, STAGES));
+      const int pre = static_cast<int>(it_end - it_begin < STAGES ? it_end - it_begin : STAGES);
       for (int st = 0; st < pre; ++st) {
         if (leader) mbar_expect_tx(&full[st], PAIR_STAGE_BYTES);
         load_b(it_begin + st, st);
