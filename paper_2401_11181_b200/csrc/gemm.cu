@@ -277,14 +277,12 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
       // ------------------------------------------------ TMA producer
       const uint64_t pol_a = l2_policy_evict_last();   // activations: reused by every n-tile
       const uint64_t pol_b = l2_policy_evict_first();  // weights: streamed once per GEMM
-      auto load_a = [&](long long i, int stage) {
-        const int ctile = static_cast<int>(i / kbs), kb = static_cast<int>(i % kbs);
+      auto load_a = [&](int ctile, int kb, int stage) {
         const int m_idx = (ctile % groups_m) * CS + rank;
         tma_load_2d(sa + stage * Cfg::A_BYTES, &tmap_a, &full[stage], kb * Cfg::BK,
                     m_idx * Cfg::BM, pol_a);
       };
-      auto load_b = [&](long long i, int stage) {
-        const int ctile = static_cast<int>(i / kbs), kb = static_cast<int>(i % kbs);
+      auto load_b = [&](int ctile, int kb, int stage) {
         const int n_idx = ctile / groups_m;
         if constexpr (CS == 1) {
           tma_load_2d(sb + stage * Cfg::B_BYTES, &tmap_b, &full[stage], kb * Cfg::BK, n_idx * BN,
@@ -297,19 +295,28 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
       // Weight tiles of the first stages do not depend on the previous kernel:
       // issue them before the programmatic-launch dependency wait.
       const int pre = static_cast<int>(it_end - it_begin < Cfg::STAGES ? it_end - it_begin : Cfg::STAGES);
+      const int tile0 = static_cast<int>(it_begin / kbs), kb0 = static_cast<int>(it_begin % kbs);
+      int ctile = tile0, kb = kb0;
       for (int st = 0; st < pre; ++st) {
         mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
-        load_b(it_begin + st, st);
+        load_b(ctile, kb, st);
+        if (++kb == kbs) { kb = 0; ++ctile; }
       }
       griddep_wait();
-      for (int st = 0; st < pre; ++st) load_a(it_begin + st, st);
+      ctile = tile0;
+      kb = kb0;
+      for (int st = 0; st < pre; ++st) {
+        load_a(ctile, kb, st);
+        if (++kb == kbs) { kb = 0; ++ctile; }
+      }
       int stage = pre % Cfg::STAGES;
       uint32_t phase = pre == Cfg::STAGES ? 1u : 0u;
       for (long long i = it_begin + pre; i < it_end; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-        load_a(i, stage);
-        load_b(i, stage);
+        load_a(ctile, kb, stage);
+        load_b(ctile, kb, stage);
+        if (++kb == kbs) { kb = 0; ++ctile; }
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
@@ -557,30 +564,39 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
     if (lane == 0) {
       const uint64_t pol_w = l2_policy_evict_first();
       const uint64_t pol_x = l2_policy_evict_last();
-      auto load_w = [&](long long i, int stage) {
-        tma_load_2d(sw + stage * Cfg::W_BYTES, &tmap_w, &full[stage],
-                    static_cast<int>(i % kbs) * Cfg::BK, static_cast<int>(i / kbs) * Cfg::BM, pol_w);
+      auto load_w = [&](int tile, int kb, int stage) {
+        tma_load_2d(sw + stage * Cfg::W_BYTES, &tmap_w, &full[stage], kb * Cfg::BK,
+                    tile * Cfg::BM, pol_w);
       };
-      auto load_x = [&](long long i, int stage) {
-        tma_load_2d(sx + stage * Cfg::X_BYTES, &tmap_x, &full[stage],
-                    static_cast<int>(i % kbs) * Cfg::BK, 0, pol_x);
+      auto load_x = [&](int tile, int kb, int stage) {
+        (void)tile;
+        tma_load_2d(sx + stage * Cfg::X_BYTES, &tmap_x, &full[stage], kb * Cfg::BK, 0, pol_x);
       };
       // the weight stream starts before the dependency wait (decode: the
       // previous kernel's tail overlaps this kernel's first weight tiles)
       const int pre = static_cast<int>(it_end - it_begin < Cfg::STAGES ? it_end - it_begin : Cfg::STAGES);
+      const int tile0 = static_cast<int>(it_begin / kbs), kb0 = static_cast<int>(it_begin % kbs);
+      int tile = tile0, kb = kb0;
       for (int st = 0; st < pre; ++st) {
         mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
-        load_w(it_begin + st, st);
+        load_w(tile, kb, st);
+        if (++kb == kbs) { kb = 0; ++tile; }
       }
       griddep_wait();
-      for (int st = 0; st < pre; ++st) load_x(it_begin + st, st);
+      tile = tile0;
+      kb = kb0;
+      for (int st = 0; st < pre; ++st) {
+        load_x(tile, kb, st);
+        if (++kb == kbs) { kb = 0; ++tile; }
+      }
       int stage = pre % Cfg::STAGES;
       uint32_t phase = pre == Cfg::STAGES ? 1u : 0u;
       for (long long i = it_begin + pre; i < it_end; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-        load_w(i, stage);
-        load_x(i, stage);
+        load_w(tile, kb, stage);
+        load_x(tile, kb, stage);
+        if (++kb == kbs) { kb = 0; ++tile; }
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
@@ -830,13 +846,11 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       const uint64_t pol_a = l2_policy_evict_last();
       const uint64_t pol_b = l2_policy_evict_first();
-      auto load_a = [&](long long i, int stage) {
-        const int ctile = static_cast<int>(i / kbs), kb = static_cast<int>(i % kbs);
+      auto load_a = [&](int ctile, int kb, int stage) {
         const int m_idx = (ctile % groups_m) * CS + rank;  // this CTA's 128-row tile
         tma_load_2d_pair(sa + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, m_idx * BM, pol_a);
       };
-      auto load_b = [&](long long i, int stage) {
-        const int ctile = static_cast<int>(i / kbs), kb = static_cast<int>(i % kbs);
+      auto load_b = [&](int ctile, int kb, int stage) {
         const int n_idx = ctile / groups_m;
         const int brow = n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS;
         uint8_t* bdst = sb + stage * BH_BYTES + pair * SLICE_BYTES;
@@ -847,19 +861,28 @@ __global__ void __launch_bounds__(192, 1)
       };
       // weight tiles first (independent of the previous kernel), then wait for it
       const int pre = static_cast<int>(it_end - it_begin < STAGES ? it_end - it_begin : STAGES);
+      const int tile0 = static_cast<int>(it_begin / kbs), kb0 = static_cast<int>(it_begin % kbs);
+      int ctile = tile0, kb = kb0;
       for (int st = 0; st < pre; ++st) {
         if (leader) mbar_expect_tx(&full[st], PAIR_STAGE_BYTES);
-        load_b(it_begin + st, st);
+        load_b(ctile, kb, st);
+        if (++kb == kbs) { kb = 0; ++ctile; }
       }
       griddep_wait();
-      for (int st = 0; st < pre; ++st) load_a(it_begin + st, st);
+      ctile = tile0;
+      kb = kb0;
+      for (int st = 0; st < pre; ++st) {
+        load_a(ctile, kb, st);
+        if (++kb == kbs) { kb = 0; ++ctile; }
+      }
       int stage = pre % STAGES;
       uint32_t phase = pre == STAGES ? 1u : 0u;
       for (long long i = it_begin + pre; i < it_end; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) mbar_expect_tx(&full[stage], PAIR_STAGE_BYTES);
-        load_a(i, stage);
-        load_b(i, stage);
+        load_a(ctile, kb, stage);
+        load_b(ctile, kb, stage);
+        if (++kb == kbs) { kb = 0; ++ctile; }
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
