@@ -209,6 +209,10 @@ int tk_chunk_attention_timed(const void* q, int32_t q_stride, void* o, const voi
                              const int32_t* block_tables, int32_t n_tokens, float scale,
                              void* stream, int32_t iters, float* avg_us);
 
+/* Debug: clock64 stamps of the chunk-attention pipeline of CTA 0, recorded
+ * only when TK_FA_VARIANT=7 (scripts/attn_trace.py).                       */
+int tk_debug_fa_trace(uint64_t* host, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,6 +123,13 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float&
   e1 = __int_as_float(__float_as_int(q1) + ((__float_as_int(y1) - 0x4B400000) << 23));
 }
 
+// Timing trace of CTA 0 (TK_FA_VARIANT=7 only): clock64 stamps per pipeline
+// event and block, read back by tk_debug_fa_trace (scripts/attn_trace.py).
+__device__ unsigned long long g_fa_trace[7 * 2 * 512];
+__device__ __forceinline__ void fa_stamp(int kind, int t, int j) {
+  if (blockIdx.x == 0 && j < 512) g_fa_trace[(kind * 2 + t) * 512 + j] = clock64();
+}
+
 struct FaParams {
   const FaPair* pairs;
   const FaUnit* units;
@@ -241,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             mbar_wait(&kv_empty[st], ((ent / kRing) & 1) ^ 1);
             mbar_expect_tx(&kv_full[st], kEntry);
+            if constexpr (EXP >= 3) fa_stamp(5 + kv, 0, ent / 2);
           }
           __syncwarp();
           if (lane < 16) {
@@ -269,13 +277,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           return smem_u32(sKV + st * kEntry);
         };
         auto issue_s = [&](int t, uint32_t k_addr) {
-          const uint32_t q_addr = smem_u32(sQ + t * kQTile);
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk)
-            umma_bf16(tmem + t * 128,
-                      umma_desc_sw128(q_addr + (kk >> 2) * kQHalf + (kk & 3) * 32),
-                      umma_desc_sw128(k_addr + (kk >> 2) * kKvHalf + (kk & 3) * 32), idesc_s,
-                      kk > 0 ? 1u : 0u);
+          umma_bf16_k128<kQHalf / 16, kKvHalf / 16>(
+              tmem + t * 128, umma_desc_sw128(smem_u32(sQ + t * kQTile)),
+              umma_desc_sw128(k_addr), idesc_s, 0u);
           umma_commit(&s_full[t]);
         };
         // block 0: S_0(0), S_1(0)
@@ -297,6 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&p_full[t], pc[t] & 1);
             ++pc[t];
             tc_fence_after();
+            if constexpr (EXP >= 3) fa_stamp(2, t, ent / 2 + j);
             if (j == 0) {
               mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
               ++oc[t];
@@ -306,11 +311,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               v_addr = entry_addr(ev);
               have_v = true;
             }
-#pragma unroll
-            for (int kk = 0; kk < kKeys / 16; ++kk)  // V: MN-major, d-halves 16 KB apart
-              umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
-                           umma_desc_sw128_mn(v_addr + kk * 2048, kKvHalf, 1024), idesc_pv,
-                           (j > 0 || kk > 0) ? 1u : 0u);
+            // V: MN-major, d-halves 16 KB apart, 16 keys (2 KB) per K step
+            umma_bf16_ts_k128(tmem + 256 + t * 128, tmem + t * 128,
+                              umma_desc_sw128_mn(v_addr, kKvHalf, 1024), idesc_pv,
+                              j > 0 ? 1u : 0u);
+            if constexpr (EXP >= 3) fa_stamp(3, t, ent / 2 + j);
             if (j == v.n[t] - 1) umma_commit(&o_full[t]);
             if (j + 1 < v.n[t]) {
               if (!have_k) {
@@ -318,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 have_k = true;
               }
               issue_s(t, k_next);
+              if constexpr (EXP >= 3) fa_stamp(4, t, ent / 2 + j);
             }
           }
           umma_commit(&kv_empty[ev % kRing]);
@@ -337,7 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int HD = p.n_heads * kD;
     const float sc = p.scale_log2;
     uint32_t s_cnt = 0, o_cnt = 0;
-    for (int u = u_begin; u < u_end; ++u) {
+    int blk_cnt = 0;  // key blocks of earlier units (trace index)
+    for (int u = u_begin; u < u_end; blk_cnt += unit_view(p, u).nblk, ++u) {
       const UnitView v = unit_view(p, u);
       const int nrows = t ? v.pr.nrows1 : v.pr.nrows0;
       const int n_t = t ? v.n[1] : v.n[0];
@@ -359,7 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&s_full[t], s_cnt & 1);
         ++s_cnt;
         tc_fence_after();
-        if constexpr (EXP == 1) {  // timing experiment: no softmax work at all
+        if constexpr (EXP >= 3) {
+          if ((warp & 3) == 0 && lane == 0) fa_stamp(0, t, blk_cnt + j);
+        }
+        if constexpr (EXP == 1 || EXP == 4) {  // timing experiment: no softmax work at all
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[t]);
@@ -450,6 +460,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
+        if constexpr (EXP >= 3) {
+          if ((warp & 3) == 0 && lane == 0) fa_stamp(1, t, blk_cnt + j);
+        }
         if (lane == 0) mbar_arrive(&p_full[t]);
       }
       // ---- epilogue: O_t -> bf16 rows (or an unnormalised partial)
@@ -665,6 +678,8 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
               : variant == 4 ? (KernFn)chunk_attn_fa_kernel<0, true>
               : variant == 5 ? (KernFn)chunk_attn_fa_kernel<4, false, 1>
               : variant == 6 ? (KernFn)chunk_attn_fa_kernel<4, false, 2>
+              : variant == 7 ? (KernFn)chunk_attn_fa_kernel<4, false, 3>
+              : variant == 8 ? (KernFn)chunk_attn_fa_kernel<4, false, 4>
                              : (KernFn)chunk_attn_fa_kernel<4, false>;
   static bool cfg = false;
   if (!cfg) {
@@ -695,4 +710,12 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   return TK_OK;
 }
 
+}  // namespace tk
+
+namespace tk {
+int fa_debug_trace(unsigned long long* host, int n) {
+  n = n < 7 * 2 * 512 ? n : 7 * 2 * 512;
+  TK_CUDA(cudaMemcpyFromSymbol(host, g_fa_trace, n * sizeof(unsigned long long)));
+  return TK_OK;
+}
 }  // namespace tk

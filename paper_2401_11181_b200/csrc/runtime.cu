@@ -1267,6 +1267,10 @@ int tk_chunk_attention_timed(const void* q, int32_t q_stride, void* o, const voi
                               iters, avg_us);
 }
 
+int tk_debug_fa_trace(uint64_t* host, int32_t n) {
+  return fa_debug_trace(reinterpret_cast<unsigned long long*>(host), n);
+}
+
 int tk_event_elapsed(tk_event* a, tk_event* b, int64_t* elapsed_ns) {
   TK_CHECK(a && b && elapsed_ns, TK_EINVAL, "tk_event_elapsed: null argument");
   float ms = 0.f;

@@ -85,6 +85,7 @@ _SIGNATURES = {
     "tk_chunk_attention": ([_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                             C.c_int32, C.POINTER(tk_slice), C.c_int32, _I32P, C.c_int32,
                             C.c_float, _P], C.c_int),
+    "tk_debug_fa_trace": ([C.POINTER(C.c_uint64), C.c_int32], C.c_int),
     "tk_chunk_attention_timed": ([_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int32, C.POINTER(tk_slice), C.c_int32, _I32P,
                                   C.c_int32, C.c_float, _P, C.c_int32, C.POINTER(C.c_float)],
