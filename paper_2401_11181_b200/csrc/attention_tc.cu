@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  griddep_wait();  // Q rows and K/V pages come from the QKV GEMM (PDL launch)
   const uint32_t tmem = *tmem_slot;
   const int u_begin = p.cta_off[blockIdx.x], u_end = p.cta_off[blockIdx.x + 1];
 
@@ -525,6 +526,7 @@ __global__ void __launch_bounds__(256)
                       const FaGroup* __restrict__ groups, int n_heads,
                       const float* __restrict__ partial) {
   griddep_launch();
+  griddep_wait();  // partials of the attention kernel
   const FaGroup g = groups[blockIdx.x >> 5];
   const int t = (blockIdx.x >> 4) & 1, rg = blockIdx.x & 15;
   const FaPair pr = pairs[g.pair];
@@ -698,12 +700,12 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   prm.n_heads = g.n_heads;
   prm.layer = layer;
   prm.scale_log2 = scale * 1.4426950408889634f;
-  kern<<<plan.n_ctas, kThreads, kSmem, s>>>(tq, tkv, prm);
+  TK_CUDA(launch_pdl(kern, dim3(plan.n_ctas), dim3(kThreads), kSmem, s, tq, tkv, prm));
   TK_CUDA(cudaGetLastError());
   note_launch();
   if (plan.n_groups > 0) {
-    fa_combine_kernel<<<plan.n_groups * 32, 256, 0, s>>>(o, pairs_dev, groups_dev, g.n_heads,
-                                                         partial);
+    TK_CUDA(launch_pdl(fa_combine_kernel, dim3(plan.n_groups * 32), dim3(256), 0, s, o,
+                       pairs_dev, groups_dev, g.n_heads, partial));
     TK_CUDA(cudaGetLastError());
     note_launch();
   }

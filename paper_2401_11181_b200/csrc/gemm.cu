@@ -1224,8 +1224,7 @@ int64_t gemm_workspace_bytes(int M, int N, int K) { return plan_gemm(M, N, K, 0)
 // while the previous kernel on the stream drains; its producer prefetches
 // weight tiles and then waits (griddepcontrol.wait) before touching activations.
 static int set_pdl(cudaLaunchAttribute* attr, int n) {
-  static const bool off = getenv("TK_NO_PDL") != nullptr;
-  if (off) return n;
+  if (!pdl_enabled()) return n;
   attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[n].val.programmaticStreamSerializationAllowed = 1;
   return n + 1;

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kNormThreads)
                 __nv_bfloat16* __restrict__ y, int cols, float eps) {
   __shared__ float red[kNormThreads / 32];
   griddep_launch();  // the GEMM that consumes y may start prefetching its weights
+  griddep_wait();    // x / delta come from the previous kernel (PDL launch)
   float* xr = x + static_cast<size_t>(blockIdx.x) * cols;
   __nv_bfloat16* yr = y + static_cast<size_t>(blockIdx.x) * cols;
   float v[kNormMaxPer];
@@ -159,14 +160,10 @@ int launch_add_norm(float* x, const __nv_bfloat16* delta, const __nv_bfloat16* w
   TK_CHECK(cols % 4 == 0 && cols <= kNormThreads * kNormMaxPer, TK_EINVAL,
            "norm: cols must be a multiple of 4 and <= 8192");
   if (rows == 0) return TK_OK;
-  if (rms) {
-    if (delta) norm_kernel<true, true><<<rows, kNormThreads, 0, s>>>(x, delta, w, nullptr, y, cols, eps);
-    else norm_kernel<true, false><<<rows, kNormThreads, 0, s>>>(x, nullptr, w, nullptr, y, cols, eps);
-  } else {
-    if (delta) norm_kernel<false, true><<<rows, kNormThreads, 0, s>>>(x, delta, w, b, y, cols, eps);
-    else norm_kernel<false, false><<<rows, kNormThreads, 0, s>>>(x, nullptr, w, b, y, cols, eps);
-  }
-  TK_CUDA(cudaGetLastError());
+  const __nv_bfloat16* bb = rms ? nullptr : b;
+  auto kern = rms ? (delta ? norm_kernel<true, true> : norm_kernel<true, false>)
+                  : (delta ? norm_kernel<false, true> : norm_kernel<false, false>);
+  TK_CUDA(launch_pdl(kern, dim3(rows), dim3(kNormThreads), 0, s, x, delta, w, bb, y, cols, eps));
   note_launch();
   return TK_OK;
 }

@@ -33,6 +33,11 @@ bool use_tc_attention(int head_dim) {
 }
 static std::atomic<int64_t> g_launches{0};
 
+bool pdl_enabled() {
+  static const bool on = getenv("TK_NO_PDL") == nullptr;
+  return on;
+}
+
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_err = msg; }
