@@ -22,6 +22,8 @@ __global__ void embed_opt_kernel(const int32_t* __restrict__ ids, const TokenMet
                                  const __nv_bfloat16* __restrict__ tok,
                                  const __nv_bfloat16* __restrict__ pos, float* __restrict__ out,
                                  int hidden) {
+  griddep_launch();
+  griddep_wait();
   const int t = blockIdx.x;
   const int id = ids[t];
   const int p = meta[t].pos + 2;  // OPTLearnedPositionalEmbedding offset
@@ -50,7 +52,8 @@ __global__ void embed_opt_kernel(const int32_t* __restrict__ ids, const TokenMet
 int launch_embed_opt(const int32_t* ids, const TokenMeta* meta, int n, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* pos_emb, float* resid, int hidden, cudaStream_t s) {
   if (n == 0) return TK_OK;
-  embed_opt_kernel<<<n, 128, 0, s>>>(ids, meta, tok_emb, pos_emb, resid, hidden);
+  TK_CUDA(launch_pdl(embed_opt_kernel, dim3(n), dim3(128), 0, s, ids, meta, tok_emb, pos_emb, resid,
+                     hidden));
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;
@@ -59,6 +62,8 @@ int launch_embed_opt(const int32_t* ids, const TokenMeta* meta, int n, const __n
 __global__ void embed_plain_kernel(const int32_t* __restrict__ ids,
                                    const __nv_bfloat16* __restrict__ tok, float* __restrict__ out,
                                    int hidden) {
+  griddep_launch();
+  griddep_wait();
   const int t = blockIdx.x;
   const __nv_bfloat16* te = tok + static_cast<size_t>(ids[t]) * hidden;
   float* o = out + static_cast<size_t>(t) * hidden;
@@ -68,7 +73,7 @@ __global__ void embed_plain_kernel(const int32_t* __restrict__ ids,
 int launch_embed_llama(const int32_t* ids, int n, const __nv_bfloat16* tok_emb, float* resid,
                        int hidden, cudaStream_t s) {
   if (n == 0) return TK_OK;
-  embed_plain_kernel<<<n, 256, 0, s>>>(ids, tok_emb, resid, hidden);
+  TK_CUDA(launch_pdl(embed_plain_kernel, dim3(n), dim3(256), 0, s, ids, tok_emb, resid, hidden));
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;
@@ -171,6 +176,8 @@ int launch_add_norm(float* x, const __nv_bfloat16* delta, const __nv_bfloat16* w
 __global__ void gather_rows_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
                                    const int32_t* __restrict__ rows, int cols,
                                    float* __restrict__ out) {
+  griddep_launch();
+  griddep_wait();
   const size_t r = static_cast<size_t>(rows[blockIdx.x]) * cols;
   float* dst = out + static_cast<size_t>(blockIdx.x) * cols;
   for (int c = threadIdx.x * 4; c < cols; c += blockDim.x * 4) {
@@ -188,7 +195,7 @@ __global__ void gather_rows_kernel(const float* __restrict__ x, const __nv_bfloa
 int launch_gather_rows_f32(const float* x, const int32_t* rows, int n, int cols, float* out,
                            cudaStream_t s, const __nv_bfloat16* delta) {
   if (n == 0) return TK_OK;
-  gather_rows_kernel<<<n, 256, 0, s>>>(x, delta, rows, cols, out);
+  TK_CUDA(launch_pdl(gather_rows_kernel, dim3(n), dim3(256), 0, s, x, delta, rows, cols, out));
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;
@@ -200,6 +207,8 @@ int launch_gather_rows_f32(const float* x, const int32_t* rows, int n, int cols,
 __global__ void kv_write_kernel(__nv_bfloat16* __restrict__ qkv, const TokenMeta* __restrict__ meta,
                                 __nv_bfloat16* __restrict__ pool, KvGeom g, int layer,
                                 float q_scale, int rope, float rope_theta) {
+  griddep_launch();
+  griddep_wait();
   const int t = blockIdx.x;
   const TokenMeta m = meta[t];
   const int HD = g.n_heads * g.head_dim;
@@ -242,7 +251,8 @@ int launch_kv_write(__nv_bfloat16* qkv, const TokenMeta* meta, int n, __nv_bfloa
                     KvGeom g, int layer, float q_scale, int rope, float rope_theta,
                     cudaStream_t s) {
   if (n == 0) return TK_OK;
-  kv_write_kernel<<<n, 256, 0, s>>>(qkv, meta, pool, g, layer, q_scale, rope, rope_theta);
+  TK_CUDA(launch_pdl(kv_write_kernel, dim3(n), dim3(256), 0, s, qkv, meta, pool, g, layer, q_scale,
+                     rope, rope_theta));
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;
@@ -673,6 +683,7 @@ __global__ void __launch_bounds__(128)
                        const int32_t* __restrict__ bt, int bt_stride,
                        const int32_t* __restrict__ ctx_lens, float scale_log2,
                        float* __restrict__ ws, int max_splits) {
+  griddep_wait();  // q / pages from the QKV GEMM + kv_write (PDL launch)
   static_assert(D == 128, "decode attention: head_dim 128");
   const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
   const int ctx = ctx_lens[b];
@@ -791,6 +802,7 @@ __global__ void decode_combine_kernel(__nv_bfloat16* __restrict__ o, int n_heads
                                       const int32_t* __restrict__ ctx_lens,
                                       const float* __restrict__ ws, int max_splits) {
   griddep_launch();
+  griddep_wait();
   const int head = blockIdx.x, b = blockIdx.y;
   const int n_splits = (ctx_lens[b] + kDecSplitTokens - 1) / kDecSplitTokens;
   if (n_splits <= 1) return;
@@ -824,15 +836,13 @@ int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16*
   if (batch == 0 || max_ctx == 0) return TK_OK;
   const int splits = (max_ctx + kDecSplitTokens - 1) / kDecSplitTokens;
   const float scale_log2 = scale * 1.4426950408889634f;
-  decode_attn_kernel<128><<<dim3(splits, g.n_heads, batch), 128, 0, s>>>(
-      q, q_stride, o, pool, g, layer, block_tables, bt_stride, ctx_lens, scale_log2,
-      static_cast<float*>(workspace), splits);
-  TK_CUDA(cudaGetLastError());
+  TK_CUDA(launch_pdl(decode_attn_kernel<128>, dim3(splits, g.n_heads, batch), dim3(128), 0, s, q,
+                     q_stride, o, pool, g, layer, block_tables, bt_stride, ctx_lens, scale_log2,
+                     static_cast<float*>(workspace), splits));
   note_launch();
   if (splits > 1) {
-    decode_combine_kernel<128><<<dim3(g.n_heads, batch), 128, 0, s>>>(
-        o, g.n_heads, ctx_lens, static_cast<const float*>(workspace), splits);
-    TK_CUDA(cudaGetLastError());
+    TK_CUDA(launch_pdl(decode_combine_kernel<128>, dim3(g.n_heads, batch), dim3(128), 0, s, o,
+                       g.n_heads, ctx_lens, static_cast<const float*>(workspace), splits));
   note_launch();
   }
   return TK_OK;
@@ -841,6 +851,8 @@ int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16*
 // ------------------------------------------------------------------ argmax
 __global__ void argmax_kernel(const float* __restrict__ x, int cols, int stride,
                               int32_t* __restrict__ out) {
+  griddep_launch();
+  griddep_wait();
   const float* row = x + static_cast<size_t>(blockIdx.x) * stride;
   float best = -INFINITY;
   int idx = 0x7fffffff;
@@ -882,7 +894,7 @@ __global__ void argmax_kernel(const float* __restrict__ x, int cols, int stride,
 int launch_argmax_strided(const float* logits, int rows, int cols, int stride, int32_t* out,
                           cudaStream_t s) {
   if (rows == 0) return TK_OK;
-  argmax_kernel<<<rows, 1024, 0, s>>>(logits, cols, stride, out);
+  TK_CUDA(launch_pdl(argmax_kernel, dim3(rows), dim3(1024), 0, s, logits, cols, stride, out));
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;
@@ -935,6 +947,8 @@ int launch_fill(__nv_bfloat16* w, int64_t n, float value, cudaStream_t s) {
 
 __global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out,
                               int ffn) {
+  griddep_launch();
+  griddep_wait();
   const int t = blockIdx.x;
   const __nv_bfloat16* row = gu + static_cast<size_t>(t) * 2 * ffn;
   for (int c = threadIdx.x; c < ffn; c += blockDim.x) {
@@ -947,7 +961,7 @@ __global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat1
 int launch_swiglu(const __nv_bfloat16* gate_up, __nv_bfloat16* out, int n, int ffn,
                   cudaStream_t s) {
   if (n == 0) return TK_OK;
-  swiglu_kernel<<<n, 256, 0, s>>>(gate_up, out, ffn);
+  TK_CUDA(launch_pdl(swiglu_kernel, dim3(n), dim3(256), 0, s, gate_up, out, ffn));
   TK_CUDA(cudaGetLastError());
   note_launch();
   return TK_OK;

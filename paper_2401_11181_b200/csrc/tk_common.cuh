@@ -202,9 +202,10 @@ __device__ __forceinline__ void cluster_sync_all() {
 // Programmatic dependent launch: block until the preceding kernel on the
 // stream has completed and its writes are visible (no-op without PDL).
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// Let the next (PDL-launched) kernel on the stream be scheduled now: it only
-// prefetches weights until its griddep_wait().  Used in kernels whose whole
-// grid is resident at once, so early dependents cannot starve them.
+// Let the next (PDL-launched) kernel on the stream be scheduled: it is launched
+// once every CTA of this grid has executed this (so it can never take the
+// slots of CTAs of this grid that have not started), and it only prefetches
+// weights until its griddep_wait().
 __device__ __forceinline__ void griddep_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
