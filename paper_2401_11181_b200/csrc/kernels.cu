@@ -95,12 +95,20 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 constexpr int kNormThreads = 256;
-constexpr int kNormMaxPer = 32;  // cols <= 8192
+constexpr int kNormMaxPer = 8;  // float4 groups per thread: cols <= 8192
 
-// kAdd: x += delta (bf16 output of the preceding O-proj / FC2 GEMM, bias
-// included) is applied first and written back, so the residual stream stays
-// fp32 while those GEMMs store bf16 instead of read-modify-writing fp32.
-template <bool kRms, bool kAdd>
+__device__ __forceinline__ float4 bf16x4_to_f4(uint2 d) {
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+// One CTA per row; thread t owns the float4 groups t, t+256, ... (PER of them,
+// compile-time so the row stays in registers).  kAdd: x += delta (bf16 output
+// of the preceding O-proj / FC2 GEMM, bias included) is applied first and
+// written back, so the residual stream stays fp32 while those GEMMs store bf16
+// instead of read-modify-writing fp32.
+template <bool kRms, bool kAdd, int PER>
 __global__ void __launch_bounds__(kNormThreads)
     norm_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
                 const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ b,
@@ -108,44 +116,57 @@ __global__ void __launch_bounds__(kNormThreads)
   __shared__ float red[kNormThreads / 32];
   griddep_launch();  // the GEMM that consumes y may start prefetching its weights
   griddep_wait();    // x / delta come from the previous kernel (PDL launch)
-  float* xr = x + static_cast<size_t>(blockIdx.x) * cols;
-  __nv_bfloat16* yr = y + static_cast<size_t>(blockIdx.x) * cols;
-  float v[kNormMaxPer];
-  int n = 0;
+  const size_t row = static_cast<size_t>(blockIdx.x) * cols;
+  float4 v[PER];
   float s = 0.f;
-  for (int c = threadIdx.x * 4; c < cols; c += kNormThreads * 4, n += 4) {
-    float4 q = *reinterpret_cast<const float4*>(xr + c);
-    if constexpr (kAdd) {
-      const uint2 d = *reinterpret_cast<const uint2*>(delta + static_cast<size_t>(blockIdx.x) * cols + c);
-      const float2 d01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d.x));
-      const float2 d23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d.y));
-      q.x += d01.x; q.y += d01.y; q.z += d23.x; q.w += d23.y;
-      *reinterpret_cast<float4*>(xr + c) = q;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = (threadIdx.x + k * kNormThreads) * 4;
+    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < cols) {
+      v[k] = *reinterpret_cast<const float4*>(x + row + c);
+      if constexpr (kAdd) {
+        const float4 d = bf16x4_to_f4(*reinterpret_cast<const uint2*>(delta + row + c));
+        v[k].x += d.x; v[k].y += d.y; v[k].z += d.z; v[k].w += d.w;
+      }
     }
-    v[n] = q.x; v[n + 1] = q.y; v[n + 2] = q.z; v[n + 3] = q.w;
-    s += q.x + q.y + q.z + q.w;
   }
+  if constexpr (kAdd) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int c = (threadIdx.x + k * kNormThreads) * 4;
+      if (c < cols) *reinterpret_cast<float4*>(x + row + c) = v[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
   float mean = 0.f;
   if (!kRms) mean = block_sum<kNormThreads>(s, red) / cols;
   float ss = 0.f;
-  for (int i = 0; i < n; ++i) {
-    const float d = v[i] - mean;
-    ss += d * d;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = (threadIdx.x + k * kNormThreads) * 4;
+    if (c < cols) {
+      const float a = v[k].x - mean, bb = v[k].y - mean, cc = v[k].z - mean, dd = v[k].w - mean;
+      ss += (a * a + bb * bb) + (cc * cc + dd * dd);
+    }
   }
   const float rstd = rsqrtf(block_sum<kNormThreads>(ss, red) / cols + eps);
-  n = 0;
-  for (int c = threadIdx.x * 4; c < cols; c += kNormThreads * 4, n += 4) {
-    float o[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float t = (v[n + j] - mean) * rstd * __bfloat162float(w[c + j]);
-      if (!kRms) t += __bfloat162float(b[c + j]);
-      o[j] = t;
+  for (int k = 0; k < PER; ++k) {
+    const int c = (threadIdx.x + k * kNormThreads) * 4;
+    if (c >= cols) continue;
+    const float4 wv = bf16x4_to_f4(*reinterpret_cast<const uint2*>(w + c));
+    float4 o = make_float4((v[k].x - mean) * rstd * wv.x, (v[k].y - mean) * rstd * wv.y,
+                           (v[k].z - mean) * rstd * wv.z, (v[k].w - mean) * rstd * wv.w);
+    if (!kRms) {
+      const float4 bv = bf16x4_to_f4(*reinterpret_cast<const uint2*>(b + c));
+      o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
     }
     uint2 pk;
-    pk.x = pack_bf16x2(o[0], o[1]);
-    pk.y = pack_bf16x2(o[2], o[3]);
-    *reinterpret_cast<uint2*>(yr + c) = pk;
+    pk.x = pack_bf16x2(o.x, o.y);
+    pk.y = pack_bf16x2(o.z, o.w);
+    *reinterpret_cast<uint2*>(y + row + c) = pk;
   }
 }
 
@@ -162,12 +183,24 @@ int launch_rmsnorm(const float* x, const __nv_bfloat16* w, __nv_bfloat16* y, int
 int launch_add_norm(float* x, const __nv_bfloat16* delta, const __nv_bfloat16* w,
                     const __nv_bfloat16* b, __nv_bfloat16* y, int rows, int cols, float eps,
                     bool rms, cudaStream_t s) {
-  TK_CHECK(cols % 4 == 0 && cols <= kNormThreads * kNormMaxPer, TK_EINVAL,
+  TK_CHECK(cols % 4 == 0 && cols <= kNormThreads * kNormMaxPer * 4, TK_EINVAL,
            "norm: cols must be a multiple of 4 and <= 8192");
   if (rows == 0) return TK_OK;
   const __nv_bfloat16* bb = rms ? nullptr : b;
-  auto kern = rms ? (delta ? norm_kernel<true, true> : norm_kernel<true, false>)
-                  : (delta ? norm_kernel<false, true> : norm_kernel<false, false>);
+  const int per = (cols + kNormThreads * 4 - 1) / (kNormThreads * 4);
+  using Fn = void (*)(float*, const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
+                      __nv_bfloat16*, int, float);
+  Fn kern = nullptr;
+#define TK_NORM_CASE(P)                                                                  \
+  case P:                                                                                \
+    kern = rms ? (delta ? norm_kernel<true, true, P> : norm_kernel<true, false, P>)      \
+               : (delta ? norm_kernel<false, true, P> : norm_kernel<false, false, P>);   \
+    break;
+  switch (per) {
+    TK_NORM_CASE(1) TK_NORM_CASE(2) TK_NORM_CASE(3) TK_NORM_CASE(4)
+    TK_NORM_CASE(5) TK_NORM_CASE(6) TK_NORM_CASE(7) TK_NORM_CASE(8)
+  }
+#undef TK_NORM_CASE
   TK_CUDA(launch_pdl(kern, dim3(rows), dim3(kNormThreads), 0, s, x, delta, w, bb, y, cols, eps));
   note_launch();
   return TK_OK;
