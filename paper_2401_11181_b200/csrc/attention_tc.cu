@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = s_full + 2;            // [2] P_t in TMEM (4 warps)
   uint64_t* o_full = p_full + 2;            // [2] last PV_t of the unit retired
   uint64_t* o_free = o_full + 2;            // [2] O_t read out (4 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+  uint64_t* p_half = o_free + 2;            // [2] first 64 keys of P_t in TMEM (4 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_half + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 8 && lane == 0) {
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 4);
+      mbar_init(&p_half[t], 4);
       mbar_init(&o_full[t], 1);
       mbar_init(&o_free[t], 4);
     }
@@ -299,8 +301,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             if (j >= v.n[t]) continue;
-            mbar_wait(&p_full[t], pc[t] & 1);
-            ++pc[t];
+            // PV_t(j) in two halves: keys 0-63 as soon as the softmax warps
+            // have stored that half of P_t, keys 64-127 after the rest
+            mbar_wait(&p_half[t], pc[t] & 1);
             tc_fence_after();
             if constexpr (EXP >= 3) fa_stamp(2, t, ent / 2 + j);
             if (j == 0) {
@@ -313,9 +316,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               have_v = true;
             }
             // V: MN-major, d-halves 16 KB apart, 16 keys (2 KB) per K step
-            umma_bf16_ts_k128(tmem + 256 + t * 128, tmem + t * 128,
-                              umma_desc_sw128_mn(v_addr, kKvHalf, 1024), idesc_pv,
-                              j > 0 ? 1u : 0u);
+            const uint64_t v_desc = umma_desc_sw128_mn(v_addr, kKvHalf, 1024);
+            umma_bf16_ts_k64(tmem + 256 + t * 128, tmem + t * 128, v_desc, idesc_pv,
+                             j > 0 ? 1u : 0u);
+            mbar_wait(&p_full[t], pc[t] & 1);
+            ++pc[t];
+            tc_fence_after();
+            umma_bf16_ts_k64(tmem + 256 + t * 128, tmem + t * 128 + 32, v_desc + 512, idesc_pv, 1u);
             if constexpr (EXP >= 3) fa_stamp(3, t, ent / 2 + j);
             if (j == v.n[t] - 1) umma_commit(&o_full[t]);
             if (j + 1 < v.n[t]) {
@@ -373,7 +380,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (EXP == 1 || EXP == 4) {  // timing experiment: no softmax work at all
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[t]);
+          if (lane == 0) {
+            mbar_arrive(&p_half[t]);
+            mbar_arrive(&p_full[t]);
+          }
           continue;
         }
         float s[kKeys];
@@ -453,6 +463,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             pk[i] = pack_bf16x2(e0, e1);
           }
           tmem_st_32x32b_x16(t_s + c * 16, pk);
+          if (c == 1) {  // keys 0-63 of P_t are in TMEM: the first PV half may start
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_half[t]);
+          }
         }
         float a0, a1, b0, b1;
         f2_split(sum2[0], a0, a1);

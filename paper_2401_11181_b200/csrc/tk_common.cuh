@@ -397,6 +397,24 @@ __device__ __forceinline__ void umma_bf16_ts_k128(uint32_t d_tmem, uint32_t a_tm
       : "memory");
 }
 
+// Four K=16 UMMAs, A in tensor memory (+8 columns per step), B MN-major SW128
+// advancing 2 KB (128 descriptor units) per step: one half of a 128-deep panel.
+__device__ __forceinline__ void umma_bf16_ts_k64(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "add.u32 a, %1, 8;\n\tadd.s64 b, %2, 128;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n\t"
+      "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n\t"
+      "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
