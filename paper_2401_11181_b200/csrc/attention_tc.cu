@@ -263,83 +263,105 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ UMMA issuer
-      constexpr uint32_t idesc_s = umma_idesc_bf16(kRows, kKeys);
-      constexpr uint32_t idesc_pv = umma_idesc_bf16(kRows, kD) | (1u << 16);  // B MN-major
-      int ent = 0, uc = 0;
-      uint32_t pc[2] = {0, 0}, oc[2] = {0, 0};
-      for (int u = u_begin; u < u_end; ++u, ++uc) {
-        const UnitView v = unit_view(p, u);
-        mbar_wait(q_full, uc & 1);
+    // ------------------------------------------------------------ UMMA issuer
+    // The whole warp runs the loop (converged, so descriptors and counters are
+    // warp-uniform and feed tcgen05.mma from uniform registers directly); one
+    // elected lane issues every tcgen05 operation.
+    constexpr uint32_t idesc_s = umma_idesc_bf16(kRows, kKeys);
+    constexpr uint32_t idesc_pv = umma_idesc_bf16(kRows, kD) | (1u << 16);  // B MN-major
+    const uint64_t q_desc[2] = {umma_desc_sw128(smem_u32(sQ)), umma_desc_sw128(smem_u32(sQ + kQTile))};
+    const uint32_t kv_base = smem_u32(sKV);
+    int ent = 0, uc = 0;
+    uint32_t pc[2] = {0, 0}, oc[2] = {0, 0};
+    for (int u = u_begin; u < u_end; ++u, ++uc) {
+      const UnitView v0 = unit_view(p, u);
+      const int nblk = __shfl_sync(0xffffffffu, v0.nblk, 0);
+      const int nt[2] = {__shfl_sync(0xffffffffu, v0.n[0], 0), __shfl_sync(0xffffffffu, v0.n[1], 0)};
+      mbar_wait(q_full, uc & 1);
+      tc_fence_after();
+      auto entry_addr = [&](int e) {
+        const int st = e % kRing;
+        mbar_wait(&kv_full[st], (e / kRing) & 1);
         tc_fence_after();
-        auto entry_addr = [&](int e) {
-          const int st = e % kRing;
-          mbar_wait(&kv_full[st], (e / kRing) & 1);
-          tc_fence_after();
-          return smem_u32(sKV + st * kEntry);
-        };
-        auto issue_s = [&](int t, uint32_t k_addr) {
-          umma_bf16_k128<kQHalf / 16, kKvHalf / 16>(
-              tmem + t * 128, umma_desc_sw128(smem_u32(sQ + t * kQTile)),
-              umma_desc_sw128(k_addr), idesc_s, 0u);
+        return kv_base + st * kEntry;
+      };
+      auto issue_s = [&](int t, uint32_t k_addr) {
+        if (elect_one_sync()) {
+          umma_bf16_k128<kQHalf / 16, kKvHalf / 16>(tmem + t * 128, q_desc[t],
+                                                     umma_desc_sw128(k_addr), idesc_s, 0u);
           umma_commit(&s_full[t]);
-        };
-        // block 0: S_0(0), S_1(0)
-        {
-          const uint32_t k_addr = entry_addr(ent);
-#pragma unroll
-          for (int t = 0; t < 2; ++t)
-            if (v.n[t] > 0) issue_s(t, k_addr);
-          umma_commit(&kv_empty[ent % kRing]);
-          if (v.nblk == 1) umma_commit(q_empty);
         }
-        for (int j = 0; j < v.nblk; ++j) {
-          const int ek = ent + 2 * j, ev = ek + 1, ek_next = ek + 2;
-          uint32_t v_addr = 0, k_next = 0;
-          bool have_v = false, have_k = false;
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one_sync()) umma_commit(bar);
+        __syncwarp();
+      };
+      // block 0: S_0(0), S_1(0)
+      {
+        const uint32_t k_addr = entry_addr(ent);
 #pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            if (j >= v.n[t]) continue;
-            // PV_t(j) in two halves: keys 0-63 as soon as the softmax warps
-            // have stored that half of P_t, keys 64-127 after the rest
-            mbar_wait(&p_half[t], pc[t] & 1);
+        for (int t = 0; t < 2; ++t)
+          if (nt[t] > 0) issue_s(t, k_addr);
+        commit(&kv_empty[ent % kRing]);
+        if (nblk == 1) commit(q_empty);
+      }
+      for (int j = 0; j < nblk; ++j) {
+        const int ek = ent + 2 * j, ev = ek + 1, ek_next = ek + 2;
+        uint32_t v_addr = 0, k_next = 0;
+        bool have_v = false, have_k = false;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (j >= nt[t]) continue;
+          // PV_t(j) in two halves: keys 0-63 as soon as the softmax warps
+          // have stored that half of P_t, keys 64-127 after the rest
+          mbar_wait(&p_half[t], pc[t] & 1);
+          tc_fence_after();
+          if constexpr (EXP >= 3) {
+            if (lane == 0) fa_stamp(2, t, ent / 2 + j);
+          }
+          if (j == 0) {
+            mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
+            ++oc[t];
             tc_fence_after();
-            if constexpr (EXP >= 3) fa_stamp(2, t, ent / 2 + j);
-            if (j == 0) {
-              mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
-              ++oc[t];
-              tc_fence_after();
-            }
-            if (!have_v) {
-              v_addr = entry_addr(ev);
-              have_v = true;
-            }
-            // V: MN-major, d-halves 16 KB apart, 16 keys (2 KB) per K step
-            const uint64_t v_desc = umma_desc_sw128_mn(v_addr, kKvHalf, 1024);
+          }
+          if (!have_v) {
+            v_addr = entry_addr(ev);
+            have_v = true;
+          }
+          // V: MN-major, d-halves 16 KB apart, 16 keys (2 KB) per K step
+          const uint64_t v_desc = umma_desc_sw128_mn(v_addr, kKvHalf, 1024);
+          if (elect_one_sync())
             umma_bf16_ts_k64(tmem + 256 + t * 128, tmem + t * 128, v_desc, idesc_pv,
                              j > 0 ? 1u : 0u);
-            mbar_wait(&p_full[t], pc[t] & 1);
-            ++pc[t];
-            tc_fence_after();
-            umma_bf16_ts_k64(tmem + 256 + t * 128, tmem + t * 128 + 32, v_desc + 512, idesc_pv, 1u);
-            if constexpr (EXP >= 3) fa_stamp(3, t, ent / 2 + j);
-            if (j == v.n[t] - 1) umma_commit(&o_full[t]);
-            if (j + 1 < v.n[t]) {
-              if (!have_k) {
-                k_next = entry_addr(ek_next);
-                have_k = true;
-              }
-              issue_s(t, k_next);
-              if constexpr (EXP >= 3) fa_stamp(4, t, ent / 2 + j);
+          __syncwarp();
+          mbar_wait(&p_full[t], pc[t] & 1);
+          ++pc[t];
+          tc_fence_after();
+          if (elect_one_sync())
+            umma_bf16_ts_k64(tmem + 256 + t * 128, tmem + t * 128 + 32, v_desc + 512, idesc_pv,
+                             1u);
+          __syncwarp();
+          if constexpr (EXP >= 3) {
+            if (lane == 0) fa_stamp(3, t, ent / 2 + j);
+          }
+          if (j == nt[t] - 1) commit(&o_full[t]);
+          if (j + 1 < nt[t]) {
+            if (!have_k) {
+              k_next = entry_addr(ek_next);
+              have_k = true;
+            }
+            issue_s(t, k_next);
+            if constexpr (EXP >= 3) {
+              if (lane == 0) fa_stamp(4, t, ent / 2 + j);
             }
           }
-          umma_commit(&kv_empty[ev % kRing]);
-          if (j + 1 < v.nblk) umma_commit(&kv_empty[ek_next % kRing]);
-          if (j + 2 == v.nblk) umma_commit(q_empty);  // the unit's last S has been issued
         }
-        ent += 2 * v.nblk;
+        commit(&kv_empty[ev % kRing]);
+        if (j + 1 < nblk) commit(&kv_empty[ek_next % kRing]);
+        if (j + 2 == nblk) commit(q_empty);  // the unit's last S has been issued
       }
+      ent += 2 * nblk;
     }
   } else {
     // -------------------------------------------------------------- softmax warps
