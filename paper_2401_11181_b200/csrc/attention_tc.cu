@@ -125,7 +125,7 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float&
 
 // Timing trace of CTA 0 (TK_FA_VARIANT=7 only): clock64 stamps per pipeline
 // event and block, read back by tk_debug_fa_trace (scripts/attn_trace.py).
-__device__ unsigned long long g_fa_trace[7 * 2 * 512];
+__device__ unsigned long long g_fa_trace[10 * 2 * 512];
 __device__ __forceinline__ void fa_stamp(int kind, int t, int j) {
   if (blockIdx.x == 0 && j < 512) g_fa_trace[(kind * 2 + t) * 512 + j] = clock64();
 }
@@ -754,7 +754,7 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
 
 namespace tk {
 int fa_debug_trace(unsigned long long* host, int n) {
-  n = n < 7 * 2 * 512 ? n : 7 * 2 * 512;
+  n = n < 10 * 2 * 512 ? n : 10 * 2 * 512;
   TK_CUDA(cudaMemcpyFromSymbol(host, g_fa_trace, n * sizeof(unsigned long long)));
   return TK_OK;
 }

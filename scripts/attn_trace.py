@@ -18,7 +18,8 @@ import torch  # noqa: E402
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2401_11181_b200 import native  # noqa: E402
 
-KINDS = ["sm_seeS", "sm_relP", "mma_seeP", "mma_PV", "mma_Snext", "prod_K", "prod_V"]
+KINDS = ["sm_seeS", "sm_relP", "mma_seeP", "mma_PV", "mma_Snext", "prod_K", "prod_V",
+         "sm_ldS", "sm_max", "sm_exp"]
 
 
 def main():
@@ -35,8 +36,8 @@ def main():
     qkv = torch.randn(512, 3 * H * D, device="cuda").bfloat16()
     native.chunk_attention_timed(qkv, 3 * H * D, pool, 1, L, H, D, [(args.prefix, 512, 0, n_pages, 1)],
                                  list(range(n_pages)), iters=3)
-    buf = (ctypes.c_uint64 * (7 * 2 * 512))()
-    native.check(native.load().tk_debug_fa_trace(buf, 7 * 2 * 512), "trace")
+    buf = (ctypes.c_uint64 * (10 * 2 * 512))()
+    native.check(native.load().tk_debug_fa_trace(buf, 10 * 2 * 512), "trace")
     get = lambda k, t, j: buf[(k * 2 + t) * 512 + j]  # noqa: E731
     base = min(v for v in buf if v) if any(buf) else 0
     print("block " + " ".join(f"{k}{t}".rjust(11) for k in KINDS[:5] for t in (0, 1)) + " "
@@ -55,6 +56,12 @@ def main():
     wait = [get(0, 0, j + 1) - get(1, 0, j) for j in range(args.first, args.first + args.count)]
     print("tile0 period", sum(per) // len(per), "softmax", sum(sm) // len(sm),
           "P->next S", sum(wait) // len(wait), "cycles (mean)")
+    rng = range(args.first, args.first + args.count)
+    if get(7, 0, args.first):
+        def mean(a, b):
+            return sum(get(b, 0, j) - get(a, 0, j) for j in rng) // len(rng)
+        print("softmax split (tile 0): S seen -> S loaded", mean(0, 7), "| -> max exchanged",
+              mean(7, 8), "| -> exps+P stores issued", mean(8, 9), "| -> P released", mean(9, 1))
 
 
 if __name__ == "__main__":
