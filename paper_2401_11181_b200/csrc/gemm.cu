@@ -326,9 +326,11 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
       griddep_wait();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------ MMA issuer (converged
+      // warp, one elected lane issues: operands stay in uniform registers)
       constexpr uint32_t idesc = umma_idesc_bf16(Cfg::BM, BN);
+      const uint32_t sa_base = smem_u32(sa), sb_base = smem_u32(sb);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -343,21 +345,23 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
         for (int k = 0; k < nkb; ++k) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sa + stage * Cfg::A_BYTES);
-          const uint32_t b_addr = smem_u32(sb + stage * Cfg::B_BYTES);
+          const uint64_t a_desc = umma_desc_sw128(sa_base + stage * Cfg::A_BYTES);
+          const uint64_t b_desc = umma_desc_sw128(sb_base + stage * Cfg::B_BYTES);
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int kk = 0; kk < Cfg::BK / 16; ++kk) {
-            umma_bf16(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
-                      idesc, (k > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < Cfg::BK / 16; ++kk)
+              umma_bf16(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+            if constexpr (CS == 1) umma_commit(&empty[stage]);
+            else umma_commit_mc(&empty[stage], kMask);
           }
-          if constexpr (CS == 1) umma_commit(&empty[stage]);
-          else umma_commit_mc(&empty[stage], kMask);
+          __syncwarp();
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        if (elect_one_sync()) umma_commit(&tfull[acc]);
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         i = seg_end;
@@ -606,8 +610,9 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
       griddep_wait();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // converged warp, one elected lane issues
       constexpr uint32_t idesc = umma_idesc_bf16(Cfg::BM, NB);
+      const uint32_t sw_base = smem_u32(sw), sx_base = smem_u32(sx);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -622,19 +627,22 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
         for (int k = 0; k < nkb; ++k) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t w_addr = smem_u32(sw + stage * Cfg::W_BYTES);
-          const uint32_t x_addr = smem_u32(sx + stage * Cfg::X_BYTES);
+          const uint64_t w_desc = umma_desc_sw128(sw_base + stage * Cfg::W_BYTES);
+          const uint64_t x_desc = umma_desc_sw128(sx_base + stage * Cfg::X_BYTES);
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int kk = 0; kk < Cfg::BK / 16; ++kk)
-            umma_bf16(d_tmem, umma_desc_sw128(w_addr + kk * 32), umma_desc_sw128(x_addr + kk * 32),
-                      idesc, (k > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&empty[stage]);
+            for (int kk = 0; kk < Cfg::BK / 16; ++kk)
+              umma_bf16(d_tmem, w_desc + 2 * kk, x_desc + 2 * kk, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+            umma_commit(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        if (elect_one_sync()) umma_commit(&tfull[acc]);
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         i = seg_end;
@@ -892,8 +900,11 @@ __global__ void __launch_bounds__(192, 1)
       griddep_wait();
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    // The leader's whole warp runs the issue loop (converged: descriptors and
+    // counters stay in uniform registers); one elected lane issues tcgen05 ops.
+    if (leader) {
       constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
+      const uint32_t sa_base = smem_u32(sa), sb_base = smem_u32(sb);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -908,19 +919,23 @@ __global__ void __launch_bounds__(192, 1)
         for (int k = 0; k < nkb; ++k) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sa + stage * A_BYTES);
-          const uint32_t b_addr = smem_u32(sb + stage * BH_BYTES);
+          const uint64_t a_desc = umma_desc_sw128(sa_base + stage * A_BYTES);
+          const uint64_t b_desc = umma_desc_sw128(sb_base + stage * BH_BYTES);
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            umma_bf16_pair(d_tmem, umma_desc_sw128(a_addr + kk * 32),
-                           umma_desc_sw128(b_addr + kk * 32), idesc, (k > 0 || kk > 0) ? 1u : 0u);
-          umma_commit_pair_mc(&empty[stage], all_mask);
+            for (int kk = 0; kk < BK / 16; ++kk)  // +32 B per K step = +2 descriptor units
+              umma_bf16_pair(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
+                             (k > 0 || kk > 0) ? 1u : 0u);
+            umma_commit_pair_mc(&empty[stage], all_mask);
+          }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair_mc(&tfull[acc], pair_mask);
+        if (elect_one_sync()) umma_commit_pair_mc(&tfull[acc], pair_mask);
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         i = seg_end;
