@@ -34,6 +34,8 @@
 #include "tk_kernels.h"
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <cstdlib>
 
 namespace tk {
@@ -1061,8 +1063,62 @@ static EncodeTiledFn encode_fn() {
 }
 
 // rows x cols bf16 row-major (cols = K contiguous), box = box_rows x 64, SW128.
+// Experiment switches, read once (getenv scans the environment: too slow per launch).
+struct GemmEnv {
+  bool no_skinny, no_pair, no_narrow;
+  int fbn = 0, fcs = 0, fdp = -1;  // TK_GEMM_CFG="BN,CS,DP"
+  GemmEnv() {
+    no_skinny = getenv("TK_NO_SKINNY") != nullptr;
+    no_pair = getenv("TK_NO_PAIR") != nullptr;
+    no_narrow = getenv("TK_NO_NARROW") != nullptr;
+    if (const char* f = getenv("TK_GEMM_CFG")) sscanf(f, "%d,%d,%d", &fbn, &fcs, &fdp);
+  }
+};
+static const GemmEnv& genv() {
+  static const GemmEnv e;
+  return e;
+}
+
+// Tensor maps are encoded once per (base, rows, cols, box): weights and the
+// runtime's activation buffers have fixed addresses, so decode steps (hundreds
+// of GEMMs each) reuse them instead of calling cuTensorMapEncodeTiled per launch.
+struct TmapKey {
+  const void* base;
+  uint64_t rows, cols;
+  uint32_t box;
+  bool operator==(const TmapKey& o) const {
+    return base == o.base && rows == o.rows && cols == o.cols && box == o.box;
+  }
+};
+struct TmapHash {
+  size_t operator()(const TmapKey& k) const {
+    return std::hash<const void*>()(k.base) ^ (k.rows * 0x9E3779B97F4A7C15ull) ^ (k.cols << 20) ^ k.box;
+  }
+};
+
+static int encode_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                         uint32_t box_rows);
+
 int make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                      uint32_t box_rows) {
+  static std::unordered_map<TmapKey, CUtensorMap, TmapHash> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  const TmapKey key{base, rows, cols, box_rows};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *map = it->second;
+    return TK_OK;
+  }
+  const int rc = encode_kmajor(map, base, rows, cols, box_rows);
+  if (rc) return rc;
+  if (cache.size() > 16384) cache.clear();  // freed buffers' addresses may be reused: bounded
+  cache.emplace(key, *map);
+  return TK_OK;
+}
+
+static int encode_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                         uint32_t box_rows) {
   EncodeTiledFn fn = encode_fn();
   TK_CHECK(fn != nullptr, TK_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {cols, rows};
@@ -1170,11 +1226,11 @@ static GemmPlan plan_skinny(int M, int N, int K, int max_ctas) {
 }
 
 static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
-  if (M <= kSkinnyMaxM && getenv("TK_NO_SKINNY") == nullptr) return plan_skinny(M, N, K, max_ctas);
+  if (M <= kSkinnyMaxM && !genv().no_skinny) return plan_skinny(M, N, K, max_ctas);
   GemmPlan pl{};
   pl.bn = pick_bn(N);
   pl.tiles_m = (M + 127) / 128;
-  pl.pair = pl.bn == 256 && pl.tiles_m % 2 == 0 && getenv("TK_NO_PAIR") == nullptr;
+  pl.pair = pl.bn == 256 && pl.tiles_m % 2 == 0 && !genv().no_pair;
   pl.cs = pl.tiles_m % 4 == 0 ? 4 : (pl.tiles_m % 2 == 0 ? 2 : 1);
   if (pl.pair && pl.cs == 1) pl.cs = 2;
   pl.kbs = K / 64;
@@ -1188,8 +1244,8 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
     // exchange over), a data-parallel schedule with one tile per cluster wins:
     // O-proj at M=512 38 -> 46 us (measured); for long K (FC2) or several
     // waves (QKV, FC1) the narrow tiles lose to their extra L2 traffic for A.
-    int fbn = 0, fcs = 0, fdp = -1;  // TK_GEMM_CFG="BN,CS,DP" forces a schedule (experiments)
-    if (const char* f = getenv("TK_GEMM_CFG")) sscanf(f, "%d,%d,%d", &fbn, &fcs, &fdp);
+    // TK_GEMM_CFG="BN,CS,DP" forces a schedule (experiments)
+    const int fbn = genv().fbn, fcs = genv().fcs, fdp = genv().fdp;
     if (fdp >= 0 && (fbn == 256 || fbn == 160) && (fcs == 2 || (fcs == 4 && pl.tiles_m % 4 == 0))) {
       pl.bn = fbn;
       pl.cs = fcs;
@@ -1202,7 +1258,7 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
         clusters = static_cast<int>(g);
         data_parallel = true;
       }
-    } else if (K <= 8192 && getenv("TK_NO_NARROW") == nullptr) {
+    } else if (K <= 8192 && !genv().no_narrow) {
       const int groups_m = pl.tiles_m / pl.cs;
       const int tn = (N + 159) / 160;
       if (tn * groups_m <= clusters && 4 * tn * groups_m >= 3 * clusters) {
@@ -1463,7 +1519,7 @@ static int dispatch_cs(const void* B, int N, int K, const CUtensorMap& ta, GemmA
   }
 }
 
-bool gemm_is_skinny(int M) { return M <= kSkinnyMaxM && getenv("TK_NO_SKINNY") == nullptr; }
+bool gemm_is_skinny(int M) { return M <= kSkinnyMaxM && !genv().no_skinny; }
 
 int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, int N, int K,
               int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas,
@@ -1477,7 +1533,16 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   TK_CHECK(N % 8 == 0, TK_EINVAL, "gemm: N must be a multiple of 8");
   static const int env_ctas = getenv("TK_GEMM_MAX_CTAS") ? atoi(getenv("TK_GEMM_MAX_CTAS")) : 0;
   if (max_ctas <= 0 && env_ctas > 0) max_ctas = env_ctas;  // experiments only
-  const GemmPlan pl = plan_gemm(M, N, K, max_ctas);
+  // plans depend only on the shape (and the experiment switches): cache them
+  static std::unordered_map<uint64_t, GemmPlan> plans;
+  static std::mutex plans_mu;
+  std::unique_lock<std::mutex> plans_lock(plans_mu);
+  const uint64_t pkey = (static_cast<uint64_t>(M) << 44) ^ (static_cast<uint64_t>(N) << 22) ^
+                        static_cast<uint64_t>(K) ^ (static_cast<uint64_t>(max_ctas) << 58);
+  auto pit = plans.find(pkey);
+  if (pit == plans.end()) pit = plans.emplace(pkey, plan_gemm(M, N, K, max_ctas)).first;
+  const GemmPlan pl = pit->second;
+  plans_lock.unlock();
   TK_CHECK(ws_bytes >= pl.ws_bytes, TK_EINVAL, "gemm: workspace too small");
   TK_CHECK(pl.counters_fit, TK_EINVAL, "gemm: too many tiles for the counter region");
   if (pl.skinny) {

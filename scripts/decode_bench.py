@@ -7,6 +7,7 @@ holds: timing only), with per-kernel-class CUDA-event profiling.
 """
 import argparse
 import json
+import time
 import sys
 from pathlib import Path
 
@@ -31,10 +32,16 @@ def main():
     for i in range(3):
         ev, _ = inst.decode_step(last, [args.ctx + i] * args.batch, bt, pages_per)
         ev.wait()
+    host = [0.0]
+    per_step = []
+
     def run(off):
         evs = []
         for i in range(args.steps):
+            t0 = time.perf_counter()
             ev, out = inst.decode_step(last, [args.ctx + off + i] * args.batch, bt, pages_per)
+            host[0] += time.perf_counter() - t0
+            per_step.append(round((time.perf_counter() - t0) * 1e3, 3))
             evs.append(ev)
         for e in evs:
             e.wait()
@@ -42,6 +49,7 @@ def main():
     # timed without per-kernel events (they would serialise the launches), then
     # once more with them for the per-class breakdown
     total_ns = run(3)
+    host_ms = host[0] * 1e3 / args.steps
     inst.profile(True)
     run(3)
     prof = inst.profile_read()
@@ -50,6 +58,8 @@ def main():
     kv = args.batch * (args.ctx + 3 + args.steps / 2) * m.kv_bytes_per_token
     print(json.dumps({
         "batch": args.batch, "ctx": args.ctx, "step_ms": round(step_ms, 3),
+        "host_enqueue_ms": round(host_ms, 3),
+        "host_first_steps_ms": per_step[:4],
         "tok_s": round(args.batch / step_ms * 1e3, 1),
         "hbm_floor_ms": round((weights + kv) / 6554.2e9 * 1e3, 3),
         "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 3) for k, v in prof.items()},
