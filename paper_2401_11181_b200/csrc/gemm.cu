@@ -1072,7 +1072,9 @@ struct GemmEnv {
     no_pair = getenv("TK_NO_PAIR") != nullptr;
     no_narrow = getenv("TK_NO_NARROW") != nullptr;
     if (const char* f = getenv("TK_GEMM_CFG")) sscanf(f, "%d,%d,%d", &fbn, &fcs, &fdp);
+    if (const char* c = getenv("TK_GEMM_MAX_CTAS")) max_ctas = atoi(c);
   }
+  int max_ctas = 0;  // TK_GEMM_MAX_CTAS: cap the CTAs (skips the split-minimising pick)
 };
 static const GemmEnv& genv() {
   static const GemmEnv e;
@@ -1271,7 +1273,10 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
   pl.tiles_n = (N + pl.bn - 1) / pl.bn;
   pl.total_iters = static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
   clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, pl.total_iters / 4)));
-  if (max_ctas <= 0 && !data_parallel) clusters = pick_clusters(pl.total_iters, pl.kbs, clusters);
+  // Long K (FC2: 320 k-blocks per tile) amortises a split tile's exchange: use
+  // every cluster; short K prefers the count with the fewest split tiles.
+  if (max_ctas <= 0 && !data_parallel && pl.kbs < 256)
+    clusters = pick_clusters(pl.total_iters, pl.kbs, clusters);
   pl.clusters = clusters;
   // most CTAs (clusters) sharing one tile, over all cluster tiles
   const long long ctiles = pl.total_iters / pl.kbs;
@@ -1289,7 +1294,9 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
   return pl;
 }
 
-int64_t gemm_workspace_bytes(int M, int N, int K) { return plan_gemm(M, N, K, 0).ws_bytes; }
+int64_t gemm_workspace_bytes(int M, int N, int K) {
+  return plan_gemm(M, N, K, genv().max_ctas).ws_bytes;
+}
 
 // Programmatic dependent launch (TK_NO_PDL=1 disables): the GEMM may start
 // while the previous kernel on the stream drains; its producer prefetches
@@ -1531,8 +1538,7 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   TK_CHECK(M > 0 && N > 0 && K > 0, TK_EINVAL, "gemm: empty problem");
   TK_CHECK(K % 64 == 0, TK_EINVAL, "gemm: K must be a multiple of 64");
   TK_CHECK(N % 8 == 0, TK_EINVAL, "gemm: N must be a multiple of 8");
-  static const int env_ctas = getenv("TK_GEMM_MAX_CTAS") ? atoi(getenv("TK_GEMM_MAX_CTAS")) : 0;
-  if (max_ctas <= 0 && env_ctas > 0) max_ctas = env_ctas;  // experiments only
+  if (max_ctas <= 0 && genv().max_ctas > 0) max_ctas = genv().max_ctas;  // experiments only
   // plans depend only on the shape (and the experiment switches): cache them
   static std::unordered_map<uint64_t, GemmPlan> plans;
   static std::mutex plans_mu;
