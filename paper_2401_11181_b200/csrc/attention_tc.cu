@@ -99,6 +99,7 @@ __device__ __forceinline__ float ex2(float x) {
 // 2^x for a pair on the FMA pipe: x = n + f (|f| <= 1/2, magic-constant
 // rounding), 2^f by a degree-5 polynomial (rel. err < 3e-6), 2^n added to the
 // exponent field.  x is clamped at -127 so masked (-inf) scores give ~0.
+template <int DEG = 5>
 __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float& e1) {
   x0 = fmaxf(x0, -127.f);
   x1 = fmaxf(x1, -127.f);
@@ -110,12 +111,21 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float&
   float n0, n1;
   f2_split(n, n0, n1);
   const uint64_t f = f2_add(x, f2(-n0, -n1));
-  uint64_t q = f2(1.3333558e-3f, 1.3333558e-3f);
-  q = f2_fma(q, f, f2(9.6181291e-3f, 9.6181291e-3f));
-  q = f2_fma(q, f, f2(5.5504109e-2f, 5.5504109e-2f));
-  q = f2_fma(q, f, f2(2.4022651e-1f, 2.4022651e-1f));
-  q = f2_fma(q, f, f2(6.9314718e-1f, 6.9314718e-1f));
-  q = f2_fma(q, f, f2(1.0f, 1.0f));
+  uint64_t q;
+  if constexpr (DEG >= 5) {
+    q = f2(1.3333558e-3f, 1.3333558e-3f);
+    q = f2_fma(q, f, f2(9.6181291e-3f, 9.6181291e-3f));
+    q = f2_fma(q, f, f2(5.5504109e-2f, 5.5504109e-2f));
+    q = f2_fma(q, f, f2(2.4022651e-1f, 2.4022651e-1f));
+    q = f2_fma(q, f, f2(6.9314718e-1f, 6.9314718e-1f));
+    q = f2_fma(q, f, f2(1.0f, 1.0f));
+  } else {
+    // degree 3 on |f| <= 1/2: rel. err < 1e-4, well below bf16 P rounding (3.9e-3)
+    q = f2(5.5855685e-2f, 5.5855685e-2f);
+    q = f2_fma(q, f, f2(2.4017581e-1f, 2.4017581e-1f));
+    q = f2_fma(q, f, f2(6.9304585e-1f, 6.9304585e-1f));
+    q = f2_fma(q, f, f2(1.0000041f, 1.0000041f));
+  }
   float q0, q1, y0, y1;
   f2_split(q, q0, q1);
   f2_split(y, y0, y1);
@@ -167,7 +177,7 @@ __device__ __forceinline__ UnitView unit_view(const FaParams& p, int u) {
   return v;
 }
 
-template <int POLY, bool LD_BATCH, int EXP = 0>
+template <int POLY, bool LD_BATCH, int EXP = 0, int DEG = 5>
 __global__ void __launch_bounds__(kThreads, 1)
     chunk_attn_fa_kernel(const __grid_constant__ CUtensorMap tmap_q,
                          const __grid_constant__ CUtensorMap tmap_kv, const FaParams p) {
@@ -476,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float x0, x1, e0, e1;
             f2_split(f2_fma(f2(s[k], s[k + 1]), sc2, nb2), x0, x1);
             if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == POLY - 1) {
-              exp2_poly2(x0, x1, e0, e1);
+              exp2_poly2<DEG>(x0, x1, e0, e1);
             } else {
               e0 = ex2(x0);
               e1 = ex2(x1);
@@ -708,7 +718,8 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   const uint64_t blocks = static_cast<uint64_t>(pool_pages) * g.n_layers * g.n_heads * 2;
   rc = make_tmap_kmajor(&tkv, pool, blocks * g.page_tokens, kD, g.page_tokens);
   if (rc) return rc;
-  // TK_FA_VARIANT (experiments): 0 poly 1/4 (default), 1 MUFU only, 2 poly 1/2,
+  // TK_FA_VARIANT (experiments): 0 degree-3 poly for 1/4 of the exponentials
+  // (default), 1 MUFU only, 2 poly 1/2,
   // 3 poly 1/4 with one wait for the four S loads, 4 MUFU only + batched loads
   static const int variant = getenv("TK_FA_VARIANT") ? atoi(getenv("TK_FA_VARIANT")) : 0;
   using KernFn = void (*)(CUtensorMap, CUtensorMap, FaParams);
@@ -720,7 +731,10 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
               : variant == 6 ? (KernFn)chunk_attn_fa_kernel<4, false, 2>
               : variant == 7 ? (KernFn)chunk_attn_fa_kernel<4, false, 3>
               : variant == 8 ? (KernFn)chunk_attn_fa_kernel<4, false, 4>
-                             : (KernFn)chunk_attn_fa_kernel<4, false>;
+              : variant == 9 ? (KernFn)chunk_attn_fa_kernel<4, false, 0, 3>
+              : variant == 10 ? (KernFn)chunk_attn_fa_kernel<3, false, 0, 3>
+              : variant == 11 ? (KernFn)chunk_attn_fa_kernel<2, false, 0, 3>
+                             : (KernFn)chunk_attn_fa_kernel<4, false, 0, 3>;
   static bool cfg = false;
   if (!cfg) {
     TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
