@@ -715,18 +715,18 @@ __global__ void __launch_bounds__(128)
                        const __nv_bfloat16* __restrict__ pool, KvGeom g, int layer,
                        const int32_t* __restrict__ bt, int bt_stride,
                        const int32_t* __restrict__ ctx_lens, float scale_log2,
-                       float* __restrict__ ws, int max_splits) {
+                       float* __restrict__ ws, int max_splits, int split_tokens) {
   griddep_wait();  // q / pages from the QKV GEMM + kv_write (PDL launch)
   static_assert(D == 128, "decode attention: head_dim 128");
   const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
   const int ctx = ctx_lens[b];
-  const int n_splits = (ctx + kDecSplitTokens - 1) / kDecSplitTokens;
+  const int n_splits = (ctx + split_tokens - 1) / split_tokens;
   if (split >= n_splits) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, dl = (lane & 15) * 8;
   const int pt = g.page_tokens;  // 16
-  const int t0 = split * kDecSplitTokens;
-  const int t1 = min(ctx, t0 + kDecSplitTokens);
+  const int t0 = split * split_tokens;
+  const int t1 = min(ctx, t0 + split_tokens);
 
   float qv[8];
   {
@@ -833,11 +833,12 @@ __global__ void __launch_bounds__(128)
 template <int D>
 __global__ void decode_combine_kernel(__nv_bfloat16* __restrict__ o, int n_heads,
                                       const int32_t* __restrict__ ctx_lens,
-                                      const float* __restrict__ ws, int max_splits) {
+                                      const float* __restrict__ ws, int max_splits,
+                                      int split_tokens) {
   griddep_launch();
   griddep_wait();
   const int head = blockIdx.x, b = blockIdx.y;
-  const int n_splits = (ctx_lens[b] + kDecSplitTokens - 1) / kDecSplitTokens;
+  const int n_splits = (ctx_lens[b] + split_tokens - 1) / split_tokens;
   if (n_splits <= 1) return;
   const float* parts = ws + (static_cast<size_t>(b) * n_heads + head) * max_splits * (D + 2);
   float M = -INFINITY;
@@ -867,15 +868,25 @@ int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16*
   TK_CHECK(ws_bytes >= decode_attention_workspace_bytes(batch, g.n_heads, g.head_dim, max_ctx),
            TK_EINVAL, "decode attention: workspace too small");
   if (batch == 0 || max_ctx == 0) return TK_OK;
-  const int splits = (max_ctx + kDecSplitTokens - 1) / kDecSplitTokens;
+  // Partition size: 256 tokens, doubled (up to 1024) while the grid keeps at
+  // least ~4 waves of CTAs -- longer partitions amortise each CTA's setup and
+  // merge, and B=128 x ctx 512 needs no combine pass at all.
+  int split_tokens = kDecSplitTokens;
+  while (split_tokens < 4 * kDecSplitTokens &&
+         static_cast<int64_t>(batch) * g.n_heads * ((max_ctx + 2 * split_tokens - 1) / (2 * split_tokens)) >=
+             4 * 5 * kNumSMs)
+    split_tokens *= 2;
+  const int splits = (max_ctx + split_tokens - 1) / split_tokens;
+  const int ws_splits = (max_ctx + kDecSplitTokens - 1) / kDecSplitTokens;  // workspace stride
   const float scale_log2 = scale * 1.4426950408889634f;
   TK_CUDA(launch_pdl(decode_attn_kernel<128>, dim3(splits, g.n_heads, batch), dim3(128), 0, s, q,
                      q_stride, o, pool, g, layer, block_tables, bt_stride, ctx_lens, scale_log2,
-                     static_cast<float*>(workspace), splits));
+                     static_cast<float*>(workspace), ws_splits, split_tokens));
   note_launch();
   if (splits > 1) {
     TK_CUDA(launch_pdl(decode_combine_kernel<128>, dim3(g.n_heads, batch), dim3(128), 0, s, o,
-                       g.n_heads, ctx_lens, static_cast<const float*>(workspace), splits));
+                       g.n_heads, ctx_lens, static_cast<const float*>(workspace), ws_splits,
+                       split_tokens));
   note_launch();
   }
   return TK_OK;
