@@ -209,6 +209,13 @@ int tk_chunk_attention_timed(const void* q, int32_t q_stride, void* o, const voi
                              const int32_t* block_tables, int32_t n_tokens, float scale,
                              void* stream, int32_t iters, float* avg_us);
 
+/* The chunk-attention work plan for a chunk's slices (host only, no device):
+ * counts = {pairs, units, ctas, pieces, split groups}; pairs[i*6..] = (slice,
+ * row0, pos0, nrows0, nrows1, key blocks); units[i*5..] = (pair, head, kb0,
+ * kb1, piece); cta_off[c] = first unit of CTA c (n_ctas + 1 entries).       */
+int tk_fa_plan(const tk_slice* slices, int32_t n_slices, int32_t n_heads, int32_t max_ctas,
+               int32_t* counts, int32_t* pairs, int32_t pair_cap, int32_t* units,
+               int32_t unit_cap, int32_t* cta_off, int32_t cta_cap);
 /* Debug: clock64 stamps of the chunk-attention pipeline of CTA 0, recorded
  * only when TK_FA_VARIANT=7 (scripts/attn_trace.py).                       */
 int tk_debug_fa_trace(uint64_t* host, int32_t n);

@@ -1272,6 +1272,36 @@ int tk_chunk_attention_timed(const void* q, int32_t q_stride, void* o, const voi
                               iters, avg_us);
 }
 
+int tk_fa_plan(const tk_slice* slices, int32_t n_slices, int32_t n_heads, int32_t max_ctas,
+               int32_t* counts, int32_t* pairs, int32_t pcap, int32_t* units, int32_t ucap,
+               int32_t* cta_off, int32_t ocap) {
+  TK_CHECK(slices && counts && pairs && units && cta_off && n_slices > 0, TK_EINVAL,
+           "tk_fa_plan: arguments");
+  FaPlan plan{};
+  std::vector<FaPair> pr(pcap);
+  std::vector<FaUnit> un(ucap);
+  std::vector<FaGroup> gr(std::max(1, ucap));
+  TK_CHECK(build_fa_plan(slices, n_slices, n_heads, max_ctas, &plan, pr.data(), pcap, un.data(),
+                         ucap, gr.data(), ucap, cta_off, ocap) == 0,
+           TK_EINVAL, "tk_fa_plan: capacity");
+  counts[0] = plan.n_pairs;
+  counts[1] = plan.n_units;
+  counts[2] = plan.n_ctas;
+  counts[3] = plan.n_pieces;
+  counts[4] = plan.n_groups;
+  for (int i = 0; i < plan.n_pairs; ++i) {
+    const FaPair& q = pr[i];
+    const int32_t v[6] = {q.slice, q.row0, q.pos0, q.nrows0, q.nrows1, q.nblk};
+    memcpy(pairs + i * 6, v, sizeof(v));
+  }
+  for (int i = 0; i < plan.n_units; ++i) {
+    const FaUnit& u = un[i];
+    const int32_t v[5] = {u.pair, u.head, u.kb0, u.kb1, u.piece};
+    memcpy(units + i * 5, v, sizeof(v));
+  }
+  return TK_OK;
+}
+
 int tk_debug_fa_trace(uint64_t* host, int32_t n) {
   return fa_debug_trace(reinterpret_cast<unsigned long long*>(host), n);
 }

@@ -86,6 +86,8 @@ _SIGNATURES = {
                             C.c_int32, C.POINTER(tk_slice), C.c_int32, _I32P, C.c_int32,
                             C.c_float, _P], C.c_int),
     "tk_debug_fa_trace": ([C.POINTER(C.c_uint64), C.c_int32], C.c_int),
+    "tk_fa_plan": ([C.POINTER(tk_slice), C.c_int32, C.c_int32, C.c_int32, _I32P, _I32P, C.c_int32,
+                    _I32P, C.c_int32, _I32P, C.c_int32], C.c_int),
     "tk_chunk_attention_timed": ([_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int32, C.POINTER(tk_slice), C.c_int32, _I32P,
                                   C.c_int32, C.c_float, _P, C.c_int32, C.POINTER(C.c_float)],
@@ -496,3 +498,22 @@ def chunk_attention_timed(q, q_stride, pool, layer, n_layers, n_heads, head_dim,
         sl, len(slices), i32(block_tables), n, scale if scale else head_dim ** -0.5,
         _stream(stream), iters, C.byref(us)), "tk_chunk_attention_timed")
     return o, us.value
+
+
+def fa_plan(slices, n_heads, max_ctas=148):
+    """Chunk-attention work plan (host only): (pairs, units, cta_off, n_pieces)."""
+    n = len(slices)
+    n_tok = sum(sl[1] for sl in slices)
+    pcap = n + n_tok // 256 + 1
+    ucap = pcap * n_heads + max_ctas + 1
+    counts = (C.c_int32 * 5)()
+    pairs = (C.c_int32 * (pcap * 6))()
+    units = (C.c_int32 * (ucap * 5))()
+    off = (C.c_int32 * (max_ctas + 1))()
+    sl = (tk_slice * n)(*[tk_slice(*x) for x in slices])
+    check(load().tk_fa_plan(sl, n, n_heads, max_ctas, counts, pairs, pcap, units, ucap, off,
+                            max_ctas + 1), "tk_fa_plan")
+    n_pairs, n_units, n_ctas, n_pieces = counts[0], counts[1], counts[2], counts[3]
+    return ([tuple(pairs[i * 6:(i + 1) * 6]) for i in range(n_pairs)],
+            [tuple(units[i * 5:(i + 1) * 5]) for i in range(n_units)],
+            list(off[:n_ctas + 1]), n_pieces)
