@@ -1549,6 +1549,10 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   if (pit == plans.end()) pit = plans.emplace(pkey, plan_gemm(M, N, K, max_ctas)).first;
   const GemmPlan pl = pit->second;
   plans_lock.unlock();
+  static const bool debug = getenv("TK_GEMM_DEBUG") != nullptr;
+  if (debug)
+    fprintf(stderr, "gemm M=%d N=%d K=%d: %s bn=%d cs=%d clusters=%d slots=%d\n", M, N, K,
+            pl.skinny ? "skinny" : pl.pair ? "pair" : "tn", pl.bn, pl.cs, pl.clusters, pl.slots);
   TK_CHECK(ws_bytes >= pl.ws_bytes, TK_EINVAL, "gemm: workspace too small");
   TK_CHECK(pl.counters_fit, TK_EINVAL, "gemm: too many tiles for the counter region");
   if (pl.skinny) {
