@@ -412,6 +412,10 @@ def run_ours(args, world, rank, local):
     inst.close()
     if world == 1 and not args.no_decode:
         line["decode"] = decode_run(args, shape, local, peaks)
+        if args.model == "opt-13b":
+            # BASELINE.json configs[4] at one GPU: Llama-2-7B-shaped large decode batches
+            line["decode"].update(decode_run(args, native.MODELS["llama-2-7b"], local, peaks,
+                                             configs=((256, 1024),), tag="llama-2-7b_"))
     if world == 1 and not args.no_serving:
         line["serving"] = serving_run(args)
     if world == 1 and not args.no_cpu_baseline:
@@ -423,12 +427,13 @@ def run_ours(args, world, rank, local):
     print(json.dumps(line))
 
 
-def decode_run(args, shape, device: int, peaks: dict) -> dict:
+def decode_run(args, shape, device: int, peaks: dict, configs=((32, 2048), (128, 512)),
+               tag: str = "") -> dict:
     """Decode steps (tk_decode_step) at a fixed batch/context: tok/s and the
     paged decode-attention kernel against the HBM roofline (CUDA events)."""
     from paper_2401_11181_b200 import native
     out = {}
-    for batch, ctx in ((32, 2048), (128, 512)):  # pools of ~55 GB each
+    for batch, ctx in configs:  # OPT-13B pools of ~55 GB each
         steps = 16
         pages_per = (ctx + steps + 3 + 16) // 16
         inst = native.Instance(shape, device=device, seed=args.seed,
@@ -452,7 +457,7 @@ def decode_run(args, shape, device: int, peaks: dict) -> dict:
         gbs = att["bytes"] / (att["ms"] / 1e3) / 1e9
         gemm_ms = sum(prof[k]["ms"] for k in ("qkv_gemm", "o_gemm", "fc1_gemm", "fc2_gemm"))
         gemm_bytes = sum(prof[k]["bytes"] for k in ("qkv_gemm", "o_gemm", "fc1_gemm", "fc2_gemm"))
-        out[f"b{batch}_ctx{ctx}"] = {
+        out[f"{tag}b{batch}_ctx{ctx}"] = {
             "decode_tok_s": round(batch * steps / (ns / 1e9), 1),
             "step_ms": round(ns / 1e6 / steps, 3),
             "attention_roofline": {"bound": "hbm", "achieved": round(gbs, 1),

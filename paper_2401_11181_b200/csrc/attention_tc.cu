@@ -59,7 +59,7 @@ constexpr int kSmem = 2 * kQTile + kRing * kEntry + kBarBytes + 1024;
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
 constexpr int kPartStride = kD + 4;       // partial row: O[128], m, l (16-byte aligned rows)
-constexpr int kMinBlocksPerCta = 3;
+constexpr int kMinBlocksPerCta = 2;
 }  // namespace
 
 int64_t fa_partial_bytes() {
@@ -650,8 +650,10 @@ int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_cta
     row += sl.len;
   }
   const long long T = per_head * n_heads;
+  static const int min_blocks = getenv("TK_FA_MIN_BLOCKS") ? atoi(getenv("TK_FA_MIN_BLOCKS"))
+                                                          : kMinBlocksPerCta;  // experiments
   int G = static_cast<int>(std::min<long long>(std::max(1, max_ctas),
-                                               std::max<long long>(1, T / kMinBlocksPerCta)));
+                                               std::max<long long>(1, T / min_blocks)));
   if (G + 1 > ocap) return -1;
   int nu = 0, piece = 0, n_groups = 0;
   long long cur = 0;
