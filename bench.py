@@ -416,6 +416,9 @@ def run_ours(args, world, rank, local):
             # BASELINE.json configs[4] at one GPU: Llama-2-7B-shaped large decode batches
             line["decode"].update(decode_run(args, native.MODELS["llama-2-7b"], local, peaks,
                                              configs=((256, 1024),), tag="llama-2-7b_"))
+    if world == 1 and not args.no_decode:
+        line["kv_handoff"] = handoff_run(args, shape, local, peaks)
+        line["predictor"] = predictor_run(args, local, peaks)
     if world == 1 and not args.no_serving:
         line["serving"] = serving_run(args)
     if world == 1 and not args.no_cpu_baseline:
@@ -468,6 +471,67 @@ def decode_run(args, shape, device: int, peaks: dict, configs=((32, 2048), (128,
             "share_of_step": {k: round(v["ms"] / (pns / 1e6), 4) for k, v in prof.items()},
         }
     return out
+
+
+def handoff_run(args, shape, device: int, peaks: dict, prompts=(512, 900, 8192)) -> dict:
+    """P->D KV handoff (tk_kv_send, pdsim/prefill.py:420-424) between two
+    instances co-located on one GPU: one copy-kernel launch per request, pages
+    scattered on both sides.  bytes = prompt pages x page bytes (costs.py:137
+    rounds to whole pages here); HBM traffic = 2 x bytes (read + write)."""
+    import random
+
+    from paper_2401_11181_b200 import costs, native
+    n_max = (max(prompts) + PAGE - 1) // PAGE
+    src = native.Instance(shape, device=device, seed=args.seed, kv_pages=n_max + 64, max_chunk=64)
+    dst = native.Instance(shape, device=device, seed=args.seed, kv_pages=n_max + 64, max_chunk=64)
+    rng = random.Random(args.seed)
+    out = {"note": "single GPU: device-local copy bounded by HBM; NVLink peer stores use the "
+                   "same kernel with a peer destination pool (not measurable on a 1-GPU box)"}
+    for n_tok in prompts:
+        n = (n_tok + PAGE - 1) // PAGE
+        sp, dp = rng.sample(range(n_max + 64), n), rng.sample(range(n_max + 64), n)
+        for _ in range(3):
+            src.kv_send(sp, dst, dp).wait()
+        evs = [src.kv_send(sp, dst, dp) for _ in range(8)]
+        for e in evs:
+            e.wait()
+        ns = sorted(e.elapsed_ns for e in evs)[len(evs) // 2]
+        nbytes = n * src.page_bytes
+        hbm = 2 * nbytes / (ns / 1e9) / 1e9
+        out[f"prompt{n_tok}"] = {
+            "pages": n, "bytes": nbytes, "device_us": round(ns / 1e3, 1),
+            "handoff_gb_s": round(nbytes / (ns / 1e9) / 1e9, 1),
+            "roofline": {"bound": "hbm", "achieved": round(hbm, 1), "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(hbm / peaks["hbm_gbs"], 4)},
+            "reference_modeled_us_nvlink300": costs.transfer_latency(
+                costs.load_calibration({"preset": "nvlink300"}), n_tok),
+        }
+    src.close(), dst.close()
+    return out
+
+
+def predictor_run(args, device: int, peaks: dict, n: int = 16, length: int = 512) -> dict:
+    """Length predictor (tk_predict, pdsim/prefill.py:99): OPT-125M-class classifier
+    over one round's prompts (16 x 512 tokens), device time."""
+    import random
+
+    from paper_2401_11181_b200 import native
+    m = native.PREDICTOR_125M
+    inst = native.Instance(m, device=device, seed=args.seed + 1, kv_pages=n * (length // PAGE) + 8,
+                           max_chunk=n * length)
+    rng = random.Random(args.seed)
+    ids = [rng.randrange(2, m.vocab) for _ in range(n * length)]
+    for _ in range(3):
+        inst.predict(ids, [length] * n, length)[0].wait()
+    evs = [inst.predict(ids, [length] * n, length)[0] for _ in range(10)]
+    ns = native.event_elapsed_ns(evs[0], evs[-1]) / (len(evs) - 1)
+    inst.close()
+    params = 12 * (4 * 768 * 768 + 2 * 768 * 3072)
+    flops = 2 * params * n * length + 4 * 768 * 12 * n * length * (length + 1) / 2
+    tf = flops / (ns / 1e9) / 1e12
+    return {"batch": n, "len": length, "device_us": round(ns / 1e3, 1),
+            "tflops": round(tf, 1), "frac_of_peak": round(tf / peaks["bf16_tflops_sustained"], 4),
+            "note": "tiny model: launch/latency bound, not tensor bound"}
 
 
 def serving_run(args) -> dict:

@@ -1011,4 +1011,67 @@ int launch_swiglu(const __nv_bfloat16* gate_up, __nv_bfloat16* out, int n, int f
   return TK_OK;
 }
 
+// ---------------------------------------------------------------- KV page copy
+// The P->D KV handoff (pdsim/prefill.py:420-424, bytes = pdsim/costs.py:137) as one
+// launch: every (page, segment) pair is a work item, CTAs stride over the items and
+// move 16-byte vectors with four loads in flight per thread.  The destination may be
+// a peer device's pool (NVLink stores; peer access is enabled at instance creation).
+// The page list travels in the kernel parameters, so no staging copy precedes it.
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(kCopyThreads)
+kv_copy_pages_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                     const __grid_constant__ PageCopyList list) {
+  const int64_t pv = list.page_vec;
+  const int64_t seg = (pv + list.parts - 1) / list.parts;
+  const int items = list.n * list.parts;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int p = it / list.parts;
+    const int64_t b = (it - p * list.parts) * seg;
+    const int64_t e = b + seg < pv ? b + seg : pv;
+    const uint4* s = src + static_cast<int64_t>(list.src[p]) * pv;
+    uint4* d = dst + static_cast<int64_t>(list.dst[p]) * pv;
+    int64_t i = b + threadIdx.x;
+    for (; i + 3 * kCopyThreads < e; i += 4 * kCopyThreads) {
+      const uint4 v0 = ld_stream(s + i), v1 = ld_stream(s + i + kCopyThreads);
+      const uint4 v2 = ld_stream(s + i + 2 * kCopyThreads), v3 = ld_stream(s + i + 3 * kCopyThreads);
+      d[i] = v0;
+      d[i + kCopyThreads] = v1;
+      d[i + 2 * kCopyThreads] = v2;
+      d[i + 3 * kCopyThreads] = v3;
+    }
+    for (; i < e; i += kCopyThreads) d[i] = ld_stream(s + i);
+  }
+}
+
+int launch_kv_copy_pages(const void* src_pool, void* dst_pool, int64_t page_bytes,
+                         const int32_t* src_pages, const int32_t* dst_pages, int n,
+                         int n_sms, cudaStream_t s) {
+  TK_CHECK(page_bytes % 16 == 0, TK_EINVAL, "kv copy: page bytes not a multiple of 16");
+  for (int i = 0; i < n; i += kCopyMaxPages) {
+    PageCopyList list;
+    list.n = n - i < kCopyMaxPages ? n - i : kCopyMaxPages;
+    list.page_vec = page_bytes / 16;
+    // ~256 KB per work item
+    const int64_t parts = (page_bytes + (256 << 10) - 1) >> 18;
+    list.parts = static_cast<int>(parts < 1 ? 1 : parts);
+    for (int j = 0; j < list.n; ++j) {
+      list.src[j] = src_pages[i + j];
+      list.dst[j] = dst_pages[i + j];
+    }
+    const int items = list.n * list.parts;
+    const int grid = items < n_sms * kCopyCtasPerSm ? items : n_sms * kCopyCtasPerSm;
+    kv_copy_pages_kernel<<<grid, kCopyThreads, 0, s>>>(
+        static_cast<const uint4*>(src_pool), static_cast<uint4*>(dst_pool), list);
+    TK_CUDA(cudaGetLastError());
+    note_launch();
+  }
+  return TK_OK;
+}
+
 }  // namespace tk

@@ -938,6 +938,10 @@ int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
   TK_CHECK(src && dst && ev_out && (n_pages == 0 || (src_pages && dst_pages)), TK_EINVAL,
            "tk_kv_send: null argument");
   TK_CHECK(src->page_bytes == dst->page_bytes, TK_EINVAL, "tk_kv_send: page geometry differs");
+  for (int i = 0; i < n_pages; ++i)
+    TK_CHECK(src_pages[i] >= 0 && src_pages[i] < src->kv_pages && dst_pages[i] >= 0 &&
+                 dst_pages[i] < dst->kv_pages,
+             TK_ECAPACITY, "tk_kv_send: page out of pool");
   TK_CUDA(cudaSetDevice(src->device));
   // order after everything already issued on the source's compute stream
   cudaEvent_t after;
@@ -949,22 +953,27 @@ int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
   int rc = new_event(src, src->s_copy, &ev);
   if (rc) return rc;
   const int64_t pb = src->page_bytes;
-  for (int i = 0; i < n_pages;) {
-    TK_CHECK(src_pages[i] >= 0 && src_pages[i] < src->kv_pages && dst_pages[i] >= 0 &&
-                 dst_pages[i] < dst->kv_pages,
-             TK_ECAPACITY, "tk_kv_send: page out of pool");
-    // coalesce runs of consecutive pages on both sides into one copy
-    int j = i + 1;
-    while (j < n_pages && src_pages[j] == src_pages[j - 1] + 1 &&
-           dst_pages[j] == dst_pages[j - 1] + 1)
-      ++j;
-    uint8_t* d = reinterpret_cast<uint8_t*>(dst->pool) + dst_pages[i] * pb;
-    const uint8_t* sp = reinterpret_cast<const uint8_t*>(src->pool) + src_pages[i] * pb;
-    if (src->device == dst->device)
-      TK_CUDA(cudaMemcpyAsync(d, sp, (j - i) * pb, cudaMemcpyDeviceToDevice, src->s_copy));
-    else
+  int peer = src->device == dst->device;
+  if (!peer) TK_CUDA(cudaDeviceCanAccessPeer(&peer, src->device, dst->device));
+  if (peer) {
+    // one copy kernel on the source GPU; a peer destination is written over NVLink
+    int sms = 0;
+    TK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, src->device));
+    rc = launch_kv_copy_pages(src->pool, dst->pool, pb, src_pages, dst_pages, n_pages, sms,
+                              src->s_copy);
+    if (rc) return rc;
+  } else {
+    for (int i = 0; i < n_pages;) {
+      // no peer path: copy engine, runs of consecutive pages coalesced
+      int j = i + 1;
+      while (j < n_pages && src_pages[j] == src_pages[j - 1] + 1 &&
+             dst_pages[j] == dst_pages[j - 1] + 1)
+        ++j;
+      uint8_t* d = reinterpret_cast<uint8_t*>(dst->pool) + dst_pages[i] * pb;
+      const uint8_t* sp = reinterpret_cast<const uint8_t*>(src->pool) + src_pages[i] * pb;
       TK_CUDA(cudaMemcpyPeerAsync(d, dst->device, sp, src->device, (j - i) * pb, src->s_copy));
-    i = j;
+      i = j;
+    }
   }
   TK_CUDA(cudaEventRecord(ev->end, src->s_copy));
   *ev_out = ev;

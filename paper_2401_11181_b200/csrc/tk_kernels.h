@@ -157,4 +157,19 @@ int launch_fill(__nv_bfloat16* w, int64_t n, float value, cudaStream_t s);
 int launch_swiglu(const __nv_bfloat16* gate_up, __nv_bfloat16* out, int n, int ffn,
                   cudaStream_t s);
 
+// KV page copy (handoff): pages src_pages[i] of src_pool -> dst_pages[i] of dst_pool,
+// one launch per kCopyMaxPages pages; dst_pool may live on a peer device.
+constexpr int kCopyThreads = 512;
+constexpr int kCopyCtasPerSm = 4;
+constexpr int kCopyMaxPages = 1024;
+struct PageCopyList {
+  int32_t n, parts;
+  int64_t page_vec;  // page bytes / 16
+  int32_t src[kCopyMaxPages];
+  int32_t dst[kCopyMaxPages];
+};
+int launch_kv_copy_pages(const void* src_pool, void* dst_pool, int64_t page_bytes,
+                         const int32_t* src_pages, const int32_t* dst_pages, int n, int n_sms,
+                         cudaStream_t s);
+
 }  // namespace tk
