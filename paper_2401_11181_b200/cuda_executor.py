@@ -127,6 +127,7 @@ class CudaExecutor:
         self.first_token: dict[int, int] = {}
         self.last_token: dict[int, int] = {}
         self.swap_host: dict[int, tuple[int, int]] = {}       # req -> (pinned ptr, pages)
+        self._streams: dict[int, dict] = {}                   # req -> streamed handoff state
         self.predictors: dict[int, native.Instance] = {}
         self.prompts: dict[int, list[int]] = {}
         self.stats = {"prefill_tokens": 0, "prefill_chunks": 0, "decode_steps": 0,
@@ -235,6 +236,37 @@ class CudaExecutor:
         ev = self.insts[src_id].kv_send(src_pages, self.insts[dst], dst_pages)
         nbytes = len(src_pages) * self.insts[src_id].page_bytes
         self.stats["kv_bytes_sent"] += nbytes
+
+        def release_src():
+            self.pools[src_id].give(src_pages)
+            self.stats["handoff_device_ns"] += ev.elapsed_ns
+
+        return _Then(ev, release_src)
+
+    def kv_stream(self, src_inst, req: Request, dst: str, start: int, end: int,
+                  final: bool) -> object:
+        """Chunk-level KV streaming: copy the pages of prompt tokens [start, end)
+        that are complete (a page straddling ``end`` goes with the next part) to
+        pages reserved in ``dst``'s receive staging on the first part.  Parts run
+        in order on the source's copy stream, each after the chunk that wrote it."""
+        src_id = src_inst.id
+        src_pages = self.tables[src_id][req.id]
+        st = self._streams.get(req.id)
+        if st is None:
+            st = self._streams[req.id] = {"sent": 0,
+                                          "dst": self.pools[dst].take(len(src_pages), dst)}
+            self.tables[dst][req.id] = st["dst"]
+        hi = len(src_pages) if final else end // self.page_tokens
+        lo = st["sent"]
+        ev = self.insts[src_id].kv_send(src_pages[lo:hi], self.insts[dst], st["dst"][lo:hi])
+        st["sent"] = max(lo, hi)
+        nbytes = max(0, hi - lo) * self.insts[src_id].page_bytes
+        self.stats["kv_bytes_sent"] += nbytes
+        if not final:
+            return ev
+        del self._streams[req.id]
+        self.tables[src_id].pop(req.id)
+        self.kv_home[req.id] = dst
 
         def release_src():
             self.pools[src_id].give(src_pages)

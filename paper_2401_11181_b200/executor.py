@@ -10,6 +10,7 @@ prefill.py chunk loop  costs.chunk_cost (prefill.py:353)    prefill_chunk
 prefill.py round       sequential_predictor_cost (:344)     predict_round
 prefill.py send_kv     costs.transfer_latency (:422)        kv_transfer
 control.py reroute     costs.transfer_latency (:341)        kv_transfer(src=None)
+prefill.py chunk done  (new: chunk-level KV streaming)      kv_stream
 decode.py boundary     decode_iter_latency (:256-258)       decode_step
 coupled.py boundary    mixed_iter_latency (:90-93)          mixed_step
 =====================  ===================================  ==========================
@@ -69,6 +70,10 @@ class SimExecutor:
 
     def kv_transfer(self, src_inst, req, dst: str) -> int:
         return costs.transfer_latency(self.params, req.prompt_len)
+
+    def kv_stream(self, src_inst, req, dst: str, start: int, end: int, final: bool) -> int:
+        """One part of a streamed handoff: prompt tokens [start, end)."""
+        return costs.transfer_latency(self.params, end - start)
 
     def decode_step(self, inst, running, kv_tokens: int, swapped_out: int,
                     swapped_in: int) -> tuple[int, int]:

@@ -81,3 +81,33 @@ def test_cuda_executor_coupled_baseline():
     assert s["device"]["decode_tokens"] == sum(r.true_decode_len for r in reqs)
     for pool in executor.pools.values():
         assert len(pool.free) == pool.n_pages
+
+
+def test_cuda_executor_chunk_kv_streaming_matches_whole_handoff():
+    """kv_streaming=chunk: pages leave after each chunk (complete pages only, the
+    straddling page with the next part); the decode side sees the same KV, so
+    the generated tokens equal the whole-request handoff's."""
+    def run(streaming, n, seed):
+        cfg = tk.config_from_dict({
+            "executor": "cuda", "kv_streaming": streaming,
+            "workload": {"class": "HPLD", "n_requests": n, "lengths": {
+                "heavy_prompt": {"median": 700, "sigma": 0.3, "lo": 520, "hi": 1000},
+                "light_decode": {"median": 8, "sigma": 0.0, "lo": 8, "hi": 8}}},
+            "cost_model": {"preset": "nvlink300", "mem_capacity_tokens": 16000},
+            "model": {"name": "tiny", "prefill_pages": 256, "staging_pages": 256,
+                      "max_decode_batch": 16}})
+        ex = make_executor(cfg)
+        res = run_experiment(cfg, seed=seed, executor=ex)
+        assert res.summary["completed"] == n
+        for iid, pool in ex.pools.items():
+            assert len(pool.free) == pool.n_pages, iid
+        return res, ex
+
+    # one request: batch of one at every step, so the decode arithmetic is identical
+    (r0, e0), (r1, e1) = run("off", 1, 0), run("chunk", 1, 0)
+    assert e1.first_token == e0.first_token and e1.last_token == e0.last_token
+    assert e1.stats["kv_bytes_sent"] == e0.stats["kv_bytes_sent"]
+    # several requests: same pages moved in total, same first tokens
+    (r0, e0), (r1, e1) = run("off", 6, 2), run("chunk", 6, 2)
+    assert e1.first_token == e0.first_token
+    assert e1.stats["kv_bytes_sent"] == e0.stats["kv_bytes_sent"]
