@@ -30,6 +30,7 @@ the round's first chunk in ``sequential`` mode (pdsim/prefill.py:338-346).
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass, field
 
 from . import costs, native
@@ -132,7 +133,8 @@ class CudaExecutor:
         self.prompts: dict[int, list[int]] = {}
         self.stats = {"prefill_tokens": 0, "prefill_chunks": 0, "decode_steps": 0,
                       "decode_tokens": 0, "kv_bytes_sent": 0, "prefill_device_ns": 0,
-                      "decode_device_ns": 0, "handoff_device_ns": 0, "predict_calls": 0}
+                      "decode_device_ns": 0, "handoff_device_ns": 0, "predict_calls": 0,
+                      "flips": 0, "flip_host_us": 0.0}
         self._req_by_id: dict[int, Request] = {r.id: r for r in (requests or [])}
 
     # -- lifecycle ---------------------------------------------------------------------
@@ -141,25 +143,41 @@ class CudaExecutor:
 
     def attach(self, inst) -> None:
         dev = self._device_of(inst.id)
-        if inst.role == "prefill":
+        if inst.id in self.insts:
+            # Instance flip (pdsim/control.py:408-482): the role changes, the device
+            # state stays -- weights, KV pool, streams and page tables are reused
+            # as they are (the pool was sized for both roles), so nothing is
+            # reloaded or reallocated.  The pages still in flight of a drained
+            # prefill instance come back to the same pool when their copies end.
+            t0 = time.perf_counter()
+            self._ensure_predictor(inst, dev)
+            self.stats["flips"] += 1
+            self.stats["flip_host_us"] += (time.perf_counter() - t0) * 1e6
+            return
+        flips = self.config.flip_policy.enabled
+        if inst.role == "prefill" and not flips:
             pages, max_rows = self.prefill_pages, self.params.chunk_size
-        elif inst.role == "decode":
+        elif inst.role == "decode" and not flips:
             pages, max_rows = self.params.capacity_pages + self.staging_pages, self.max_batch
-        else:  # coupled: prefill + decode share one pool
-            pages = self.params.capacity_pages + self.staging_pages
+        else:  # coupled (prefill + decode share one pool), or either role after a flip
+            pages = max(self.params.capacity_pages + self.staging_pages,
+                        self.prefill_pages if flips else 0)
             max_rows = max(self.params.chunk_size, self.max_batch)
         self.insts[inst.id] = native.Instance(self.shape, device=dev, seed=self.seed,
                                               kv_pages=pages, page_tokens=self.page_tokens,
                                               max_chunk=max_rows)
         self.pools[inst.id] = _Pool(pages)
         self.tables[inst.id] = {}
+        self._ensure_predictor(inst, dev)
+
+    def _ensure_predictor(self, inst, dev: int) -> None:
         if inst.role == "prefill" and self.device_predictor and dev not in self.predictors:
             self.predictors[dev] = native.Instance(native.PREDICTOR_125M, device=dev,
                                                    seed=self.seed + 1, kv_pages=16 * 32 + 8,
                                                    max_chunk=16 * 512)
 
     def detach(self, inst) -> None:
-        pass  # device state is kept; flips reuse the id with a new role object
+        pass  # device state is kept; the flipped id re-attaches with its new role
 
     def close(self) -> None:
         for i in list(self.insts.values()) + list(self.predictors.values()):

@@ -111,3 +111,33 @@ def test_cuda_executor_chunk_kv_streaming_matches_whole_handoff():
     (r0, e0), (r1, e1) = run("off", 6, 2), run("chunk", 6, 2)
     assert e1.first_token == e0.first_token
     assert e1.stats["kv_bytes_sent"] == e0.stats["kv_bytes_sent"]
+
+
+def test_cuda_executor_flip_keeps_device_state(tmp_path):
+    """Instance flips on the device (pdsim/control.py:408-482; reference test
+    tests/test_control.py:145-157 on its two-wave trace): the role changes
+    without a new device instance -- same weights, pool and streams -- and every
+    request completes and every page returns to its pool."""
+    lines = ["arrival_us,prompt_len,decode_len"]
+    for wave in (0, 1_500_000):
+        lines += [f"{wave},{20 + i},{10 + i}" for i in range(8)]
+    trace = tmp_path / "waves.csv"
+    trace.write_text("\n".join(lines) + "\n")
+    cfg = tk.config_from_dict({
+        "executor": "cuda", "cluster": {"prefill": 2, "decode": 2},
+        "workload": {"class": "Trace", "trace_path": str(trace)},
+        "flip": {"enabled": True, "threshold": 0.5, "window_us": 400_000},
+        "cost_model": {"preset": "nvlink300", "mem_capacity_tokens": 4096},
+        "model": {"name": "tiny", "prefill_pages": 128, "staging_pages": 64,
+                  "max_decode_batch": 16}})
+    ex = make_executor(cfg)
+    res = run_experiment(cfg, seed=4, executor=ex)
+    handles = {k: id(v) for k, v in ex.insts.items()}
+    assert res.summary["completed"] == 16
+    assert res.summary["flips_completed"] >= 1
+    assert ex.stats["flips"] == res.summary["flips_completed"]
+    assert set(handles) == {"p0", "p1", "d0", "d1"}  # no instance created by a flip
+    for rec in res.control.flip_records:
+        assert 5_000 <= rec.latency_us <= 7_000
+    for iid, pool in ex.pools.items():
+        assert len(pool.free) == pool.n_pages, iid
