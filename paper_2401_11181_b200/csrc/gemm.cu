@@ -65,6 +65,7 @@ struct GemmArgs {
   int epi;
   int tiles_m, tiles_n, kbs;
   long long total_iters;
+  int b_pol;      // weights' L2 policy: 0 evict_first (read once), 1 evict_normal, 2 evict_last
   QkvScatter kv;  // EPI_QKV_PAGED only
 };
 
@@ -855,7 +856,9 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_a = l2_policy_evict_last();
-      const uint64_t pol_b = l2_policy_evict_first();
+      const uint64_t pol_b = p.b_pol == 0   ? l2_policy_evict_first()
+                             : p.b_pol == 1 ? l2_policy_evict_normal()
+                                            : l2_policy_evict_last();
       auto load_a = [&](int ctile, int kb, int stage) {
         const int m_idx = (ctile % groups_m) * CS + rank;  // this CTA's 128-row tile
         tma_load_2d_pair(sa + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, m_idx * BM, pol_a);
@@ -1067,11 +1070,13 @@ static EncodeTiledFn encode_fn() {
 struct GemmEnv {
   bool no_skinny, no_pair, no_narrow;
   int fbn = 0, fcs = 0, fdp = -1;  // TK_GEMM_CFG="BN,CS,DP"
+  int bpol = -1;                    // TK_GEMM_BPOL: weights' L2 policy (experiments)
   GemmEnv() {
     no_skinny = getenv("TK_NO_SKINNY") != nullptr;
     no_pair = getenv("TK_NO_PAIR") != nullptr;
     no_narrow = getenv("TK_NO_NARROW") != nullptr;
     if (const char* f = getenv("TK_GEMM_CFG")) sscanf(f, "%d,%d,%d", &fbn, &fcs, &fdp);
+    if (const char* f = getenv("TK_GEMM_BPOL")) bpol = atoi(f);
     if (const char* c = getenv("TK_GEMM_MAX_CTAS")) max_ctas = atoi(c);
   }
   int max_ctas = 0;  // TK_GEMM_MAX_CTAS: cap the CTAs (skips the split-minimising pick)
@@ -1597,6 +1602,9 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   a.tiles_n = pl.tiles_n;
   a.kbs = pl.kbs;
   a.cs = pl.cs;
+  // weights: evict first (measured best for every schedule, also 2-CTA clusters whose
+  // two m-groups both read each weight tile; TK_GEMM_BPOL overrides)
+  a.b_pol = genv().bpol >= 0 ? genv().bpol : 0;
   a.slots = pl.slots;
   a.total_iters = pl.total_iters;
   const int64_t tiles = static_cast<int64_t>(a.tiles_m) * a.tiles_n;
