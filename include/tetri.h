@@ -219,6 +219,10 @@ int tk_fa_plan(const tk_slice* slices, int32_t n_slices, int32_t n_heads, int32_
 /* Debug: clock64 stamps of the chunk-attention pipeline of CTA 0, recorded
  * only when TK_FA_VARIANT=7 (scripts/attn_trace.py).                       */
 int tk_debug_fa_trace(uint64_t* host, int32_t n);
+/* GEMM pipeline stamps (TK_GEMM_TRACE=1 runs): 6 kinds x 1024 k-blocks of CTA 0. */
+int tk_debug_gemm_trace(uint64_t* host, int32_t n);
+/* Per-CTA globaltimer stamps of the last traced GEMM: 5 kinds x 256 CTAs. */
+int tk_debug_gemm_cta_trace(uint64_t* host, int32_t n);
 
 #ifdef __cplusplus
 }

@@ -66,8 +66,47 @@ struct GemmArgs {
   int tiles_m, tiles_n, kbs;
   long long total_iters;
   int b_pol;      // weights' L2 policy: 0 evict_first (read once), 1 evict_normal, 2 evict_last
+  int pf_dist;    // k-blocks of weight L2 prefetch ahead of the TMA ring (0: none)
+  int wait_mode;  // TK_GEMM_WAIT: 0 all lanes poll, 1 lane 0 polls, 2 + epilogue back-off
+  int exp;        // TK_GEMM_EXP (experiments): 1 no MMAs, 2 A loads only, 3 B loads only
+  int trace;      // TK_GEMM_TRACE: clock64 stamps of CTA 0's pipeline (tk_debug_gemm_trace)
   QkvScatter kv;  // EPI_QKV_PAGED only
 };
+
+// Pipeline stamps of CTA 0 (experiments; scripts/gemm_trace.py): kind x k-block.
+//   0 issuer before full-wait, 1 after it, 2 after the k-block's MMAs + commit,
+//   3 producer before empty-wait, 4 after it, 5 epilogue saw the accumulator (per tile)
+constexpr int kGemmTraceN = 1024;
+__device__ unsigned long long g_gemm_trace[6 * kGemmTraceN];
+__device__ __forceinline__ void gemm_stamp(const GemmArgs& p, int kind, long long j) {
+  if (p.trace && blockIdx.x == 0 && j < kGemmTraceN) g_gemm_trace[kind * kGemmTraceN + j] = clock64();
+}
+
+// Per-CTA globaltimer stamps (ns): 0 entry, 1 issuer saw the first stage, 2 last
+// MMA commit issued (leaders), 3 epilogue done, 4 exit.
+__device__ unsigned long long g_gemm_cta[5 * 256];
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void gemm_cta_stamp(const GemmArgs& p, int kind) {
+  if (p.trace && blockIdx.x < 256) g_gemm_cta[kind * 256 + blockIdx.x] = globaltimer_ns();
+}
+
+int gemm_debug_cta_trace(unsigned long long* host, int n) {
+  TK_CHECK(n <= 5 * 256, TK_EINVAL, "gemm cta trace: n too large");
+  TK_CUDA(cudaDeviceSynchronize());
+  TK_CUDA(cudaMemcpyFromSymbol(host, g_gemm_cta, n * sizeof(unsigned long long)));
+  return TK_OK;
+}
+
+int gemm_debug_trace(unsigned long long* host, int n) {
+  TK_CHECK(n <= 6 * kGemmTraceN, TK_EINVAL, "gemm trace: n too large");
+  TK_CUDA(cudaDeviceSynchronize());
+  TK_CUDA(cudaMemcpyFromSymbol(host, g_gemm_trace, n * sizeof(unsigned long long)));
+  return TK_OK;
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -813,6 +852,7 @@ __global__ void __launch_bounds__(192, 1)
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) gemm_cta_stamp(p, 0);
   const int rank = static_cast<int>(cluster_ctarank());
   const int pair = rank >> 1;
   const int half = rank & 1;
@@ -859,11 +899,15 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t pol_b = p.b_pol == 0   ? l2_policy_evict_first()
                              : p.b_pol == 1 ? l2_policy_evict_normal()
                                             : l2_policy_evict_last();
+      const int xbytes = p.exp == 2 ? 2 * A_BYTES : p.exp == 3 ? PAIR_STAGE_BYTES - 2 * A_BYTES
+                                                                : PAIR_STAGE_BYTES;
       auto load_a = [&](int ctile, int kb, int stage) {
+        if (p.exp == 3) return;
         const int m_idx = (ctile % groups_m) * CS + rank;  // this CTA's 128-row tile
         tma_load_2d_pair(sa + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, m_idx * BM, pol_a);
       };
       auto load_b = [&](int ctile, int kb, int stage) {
+        if (p.exp == 2) return;
         const int n_idx = ctile / groups_m;
         const int brow = n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS;
         uint8_t* bdst = sb + stage * BH_BYTES + pair * SLICE_BYTES;
@@ -872,15 +916,31 @@ __global__ void __launch_bounds__(192, 1)
         else
           tma_load_2d_pair_mc(bdst, &tmap_b, &full[stage], kb * BK, brow, half_mask, pol_b);
       };
+      // optional L2 prefetch of this CTA's weight slice ahead of the ring (TK_GEMM_PF;
+      // measured slower, off by default)
+      const int pf_dist = p.pf_dist;
+      int pf_tile = 0, pf_kb = 0;
+      long long pf_i = it_begin;
+      auto prefetch_b_upto = [&](long long upto) {
+        for (; pf_i < upto && pf_i < it_end; ++pf_i) {
+          const int n_idx = pf_tile / groups_m;
+          tma_prefetch_2d(&tmap_b, pf_kb * BK, n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS);
+          if (++pf_kb == kbs) { pf_kb = 0; ++pf_tile; }
+        }
+      };
       // weight tiles first (independent of the previous kernel), then wait for it
       const int pre = static_cast<int>(it_end - it_begin < STAGES ? it_end - it_begin : STAGES);
       const int tile0 = static_cast<int>(it_begin / kbs), kb0 = static_cast<int>(it_begin % kbs);
       int ctile = tile0, kb = kb0;
       for (int st = 0; st < pre; ++st) {
-        if (leader) mbar_expect_tx(&full[st], PAIR_STAGE_BYTES);
+        if (leader) mbar_expect_tx(&full[st], xbytes);
         load_b(ctile, kb, st);
         if (++kb == kbs) { kb = 0; ++ctile; }
       }
+      pf_tile = ctile;
+      pf_kb = kb;
+      pf_i = it_begin + pre;
+      if (pf_dist > 0) prefetch_b_upto(it_begin + pre + pf_dist);
       griddep_wait();
       ctile = tile0;
       kb = kb0;
@@ -891,8 +951,11 @@ __global__ void __launch_bounds__(192, 1)
       int stage = pre % STAGES;
       uint32_t phase = pre == STAGES ? 1u : 0u;
       for (long long i = it_begin + pre; i < it_end; ++i) {
+        if (pf_dist > 0) prefetch_b_upto(i + pf_dist + 1);
+        gemm_stamp(p, 3, i - it_begin);
         mbar_wait(&empty[stage], phase ^ 1);
-        if (leader) mbar_expect_tx(&full[stage], PAIR_STAGE_BYTES);
+        gemm_stamp(p, 4, i - it_begin);
+        if (leader) mbar_expect_tx(&full[stage], xbytes);
         load_a(ctile, kb, stage);
         load_b(ctile, kb, stage);
         if (++kb == kbs) { kb = 0; ++ctile; }
@@ -918,20 +981,28 @@ __global__ void __launch_bounds__(192, 1)
         const int ctile = static_cast<int>(i / kbs);
         const long long seg_end = min(it_end, static_cast<long long>(ctile + 1) * kbs);
         const int nkb = static_cast<int>(seg_end - i);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (p.wait_mode) mbar_wait_lane0(&tempty[acc], acc_phase ^ 1); else mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
         for (int k = 0; k < nkb; ++k) {
-          mbar_wait(&full[stage], phase);
+          if (lane == 0) gemm_stamp(p, 0, i - it_begin + k);
+          if (p.wait_mode) mbar_wait_lane0(&full[stage], phase); else mbar_wait(&full[stage], phase);
+          if (lane == 0) {
+            gemm_stamp(p, 1, i - it_begin + k);
+            if (i - it_begin + k == 0) gemm_cta_stamp(p, 1);
+          }
           tc_fence_after();
           const uint64_t a_desc = umma_desc_sw128(sa_base + stage * A_BYTES);
           const uint64_t b_desc = umma_desc_sw128(sb_base + stage * BH_BYTES);
           if (elect_one_sync()) {
+            if (p.exp != 1) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)  // +32 B per K step = +2 descriptor units
-              umma_bf16_pair(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
-                             (k > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < BK / 16; ++kk)  // +32 B per K step = +2 descriptor units
+                umma_bf16_pair(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
+                               (k > 0 || kk > 0) ? 1u : 0u);
+            }
             umma_commit_pair_mc(&empty[stage], all_mask);
+            gemm_stamp(p, 2, i - it_begin + k);
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -941,6 +1012,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         if (elect_one_sync()) umma_commit_pair_mc(&tfull[acc], pair_mask);
         __syncwarp();
+        if (lane == 0 && seg_end == it_end) gemm_cta_stamp(p, 2);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         i = seg_end;
@@ -973,7 +1045,8 @@ __global__ void __launch_bounds__(192, 1)
             if (col_base + c < p.N) prefetch_l2(seg + c);
         }
       }
-      mbar_wait(&tfull[acc], acc_phase);
+      if (p.wait_mode == 2) mbar_wait_sleep(&tfull[acc], acc_phase); else if (p.wait_mode) mbar_wait_lane0(&tfull[acc], acc_phase); else mbar_wait(&tfull[acc], acc_phase);
+      if (ep_leader) gemm_stamp(p, 5, (i - it_begin) / kbs);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((quarter * 32) << 16) + acc * 256;
       auto release_tmem = [&]() {
@@ -1036,11 +1109,13 @@ __global__ void __launch_bounds__(192, 1)
       if (acc == 0) acc_phase ^= 1;
       i = seg_end;
     }
+    if (ep_leader) gemm_cta_stamp(p, 3);
   }
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
   if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+  if (threadIdx.x == 0) gemm_cta_stamp(p, 4);
 }
 
 
@@ -1071,12 +1146,20 @@ struct GemmEnv {
   bool no_skinny, no_pair, no_narrow;
   int fbn = 0, fcs = 0, fdp = -1;  // TK_GEMM_CFG="BN,CS,DP"
   int bpol = -1;                    // TK_GEMM_BPOL: weights' L2 policy (experiments)
+  bool trace = false;               // TK_GEMM_TRACE: pipeline stamps (experiments)
+  int pf = -1;                      // TK_GEMM_PF: weight prefetch distance (k-blocks)
+  int exp = 0;                      // TK_GEMM_EXP: pipeline experiments (wrong results)
+  int wait_mode = -1;               // TK_GEMM_WAIT
   GemmEnv() {
     no_skinny = getenv("TK_NO_SKINNY") != nullptr;
     no_pair = getenv("TK_NO_PAIR") != nullptr;
     no_narrow = getenv("TK_NO_NARROW") != nullptr;
     if (const char* f = getenv("TK_GEMM_CFG")) sscanf(f, "%d,%d,%d", &fbn, &fcs, &fdp);
     if (const char* f = getenv("TK_GEMM_BPOL")) bpol = atoi(f);
+    trace = getenv("TK_GEMM_TRACE") != nullptr;
+    if (const char* f = getenv("TK_GEMM_PF")) pf = atoi(f);
+    if (const char* f = getenv("TK_GEMM_EXP")) exp = atoi(f);
+    if (const char* f = getenv("TK_GEMM_WAIT")) wait_mode = atoi(f);
     if (const char* c = getenv("TK_GEMM_MAX_CTAS")) max_ctas = atoi(c);
   }
   int max_ctas = 0;  // TK_GEMM_MAX_CTAS: cap the CTAs (skips the split-minimising pick)
@@ -1605,6 +1688,10 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   // weights: evict first (measured best for every schedule, also 2-CTA clusters whose
   // two m-groups both read each weight tile; TK_GEMM_BPOL overrides)
   a.b_pol = genv().bpol >= 0 ? genv().bpol : 0;
+  a.trace = genv().trace ? 1 : 0;
+  a.pf_dist = genv().pf >= 0 ? genv().pf : 0;
+  a.exp = genv().exp;
+  a.wait_mode = genv().wait_mode >= 0 ? genv().wait_mode : 0;
   a.slots = pl.slots;
   a.total_iters = pl.total_iters;
   const int64_t tiles = static_cast<int64_t>(a.tiles_m) * a.tiles_n;

@@ -1311,6 +1311,14 @@ int tk_fa_plan(const tk_slice* slices, int32_t n_slices, int32_t n_heads, int32_
   return TK_OK;
 }
 
+int tk_debug_gemm_trace(uint64_t* host, int32_t n) {
+  return gemm_debug_trace(reinterpret_cast<unsigned long long*>(host), n);
+}
+
+int tk_debug_gemm_cta_trace(uint64_t* host, int32_t n) {
+  return gemm_debug_cta_trace(reinterpret_cast<unsigned long long*>(host), n);
+}
+
 int tk_debug_fa_trace(uint64_t* host, int32_t n) {
   return fa_debug_trace(reinterpret_cast<unsigned long long*>(host), n);
 }

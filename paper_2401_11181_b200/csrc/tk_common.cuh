@@ -74,6 +74,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// One lane polls, the warp follows: 32 lanes spinning on try_wait contend for the
+// barrier unit with the TMA / MMA arrivals on the same CTA's barriers.
+__device__ __forceinline__ void mbar_wait_lane0(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
+}
+
+// Poll with a back-off sleep (waits off the critical path, e.g. epilogue warps
+// waiting through a whole mainloop).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(128);
+  }
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -127,6 +143,14 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map
 // of a CTA-local shared address selects the odd CTA of a pair; clearing it
 // addresses the same offset in the even (leader) CTA.
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
+
+// L2 prefetch of one 2-D box (no shared memory, no barrier): pulls a tile that a
+// later TMA load will read from DRAM into L2 ahead of the shared-memory ring.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,
                                                  int32_t c0, int32_t c1, uint64_t policy) {

@@ -127,6 +127,8 @@ int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_cta
                   FaPair* pairs, int pcap, FaUnit* units, int ucap, FaGroup* groups, int gcap,
                   int32_t* cta_off, int ocap);
 int64_t fa_partial_bytes();
+int gemm_debug_trace(unsigned long long* host, int n);
+int gemm_debug_cta_trace(unsigned long long* host, int n);
 int fa_debug_trace(unsigned long long* host, int n);  // TK_FA_VARIANT=7 timing stamps
 int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride,
                               __nv_bfloat16* o, const __nv_bfloat16* pool, int pool_pages,

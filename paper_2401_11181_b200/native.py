@@ -86,6 +86,8 @@ _SIGNATURES = {
                             C.c_int32, C.POINTER(tk_slice), C.c_int32, _I32P, C.c_int32,
                             C.c_float, _P], C.c_int),
     "tk_debug_fa_trace": ([C.POINTER(C.c_uint64), C.c_int32], C.c_int),
+    "tk_debug_gemm_trace": ([C.POINTER(C.c_uint64), C.c_int32], C.c_int),
+    "tk_debug_gemm_cta_trace": ([C.POINTER(C.c_uint64), C.c_int32], C.c_int),
     "tk_fa_plan": ([C.POINTER(tk_slice), C.c_int32, C.c_int32, C.c_int32, _I32P, _I32P, C.c_int32,
                     _I32P, C.c_int32, _I32P, C.c_int32], C.c_int),
     "tk_chunk_attention_timed": ([_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32,
