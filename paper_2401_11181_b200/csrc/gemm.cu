@@ -67,6 +67,9 @@ struct GemmArgs {
   long long total_iters;
   int b_pol;      // weights' L2 policy: 0 evict_first (read once), 1 evict_normal, 2 evict_last
   int pf_dist;    // k-blocks of weight L2 prefetch ahead of the TMA ring (0: none)
+  int pf_partials;  // TK_GEMM_PFPART: L2-prefetch a final piece's partials (measured: no gain)
+  int stage_epi;  // last tile's bf16 epilogue staged in shared memory (TK_GEMM_STAGE_EPI=0: off)
+  int fix_depth;  // stream-K fixup: partial chunks in flight (1, or 2 = fixup_epilogue_deep)
   int wait_mode;  // TK_GEMM_WAIT: 0 all lanes poll, 1 lane 0 polls, 2 + epilogue back-off
   int exp;        // TK_GEMM_EXP (experiments): 1 no MMAs, 2 A loads only, 3 B loads only
   int trace;      // TK_GEMM_TRACE: clock64 stamps of CTA 0's pipeline (tk_debug_gemm_trace)
@@ -83,8 +86,9 @@ __device__ __forceinline__ void gemm_stamp(const GemmArgs& p, int kind, long lon
 }
 
 // Per-CTA globaltimer stamps (ns): 0 entry, 1 issuer saw the first stage, 2 last
-// MMA commit issued (leaders), 3 epilogue done, 4 exit.
-__device__ unsigned long long g_gemm_cta[5 * 256];
+// MMA commit issued (leaders), 3 epilogue done, 4 exit, 5 epilogue saw the last
+// accumulator, 6 last fixup's partials ready.
+__device__ unsigned long long g_gemm_cta[7 * 256];
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -95,7 +99,7 @@ __device__ __forceinline__ void gemm_cta_stamp(const GemmArgs& p, int kind) {
 }
 
 int gemm_debug_cta_trace(unsigned long long* host, int n) {
-  TK_CHECK(n <= 5 * 256, TK_EINVAL, "gemm cta trace: n too large");
+  TK_CHECK(n <= 7 * 256, TK_EINVAL, "gemm cta trace: n too large");
   TK_CUDA(cudaDeviceSynchronize());
   TK_CUDA(cudaMemcpyFromSymbol(host, g_gemm_cta, n * sizeof(unsigned long long)));
   return TK_OK;
@@ -120,6 +124,28 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 __host__ __device__ __forceinline__ int owner_of(long long it, long long T, int G) {
   // CTA c covers [floor(c*T/G), floor((c+1)*T/G))
   return static_cast<int>(((it + 1) * G + T - 1) / T) - 1;
+}
+
+// Bias (+ ReLU) of a 32-column chunk, for the shared-memory-staged bf16 epilogue.
+template <int EPI>
+__device__ __forceinline__ void epilogue_math(const GemmArgs& p, int col0, float (&v)[32]) {
+  if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_RELU) {
+    if (p.bias != nullptr) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        if (col0 + g * 8 < p.N) {
+          uint4 braw = __ldg(reinterpret_cast<const uint4*>(p.bias + col0 + g * 8));
+          const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&braw);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[g * 8 + j] += __bfloat162float(b[j]);
+        }
+      }
+    }
+  }
+  if constexpr (EPI == EPI_BF16_BIAS_RELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
 }
 
 template <int EPI>
@@ -255,6 +281,34 @@ __device__ __forceinline__ void fixup_epilogue(const GemmArgs& p, uint32_t t_row
 #pragma unroll
       for (int g = 0; g < 8; ++g) cur[g] = nxt[g];
     }
+  }
+}
+
+// Same, with the partial loads of chunks c+1 and c+2 in flight while chunk c is
+// finished (the fixup at the end of a stream-K range is load-latency bound).
+template <int EPI, int NCHUNK>
+__device__ __forceinline__ void fixup_epilogue_deep(const GemmArgs& p, uint32_t t_row, int row,
+                                                    int col_base, const float* tile_ws,
+                                                    size_t slot_elems, int n_slots, int tid) {
+  float4 buf[3][8];
+  partial_load(tile_ws, slot_elems, n_slots, 0, tid, buf[0]);
+  if (NCHUNK > 1) partial_load(tile_ws, slot_elems, n_slots, 1, tid, buf[1]);
+#pragma unroll
+  for (int c = 0; c < NCHUNK; ++c) {
+    if (c + 2 < NCHUNK) partial_load(tile_ws, slot_elems, n_slots, c + 2, tid, buf[(c + 2) % 3]);
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(t_row + c * 32, r);
+    tmem_wait_ld();
+    float v[32];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const float4 q = buf[c % 3][g];
+      v[g * 4] = __uint_as_float(r[g * 4]) + q.x;
+      v[g * 4 + 1] = __uint_as_float(r[g * 4 + 1]) + q.y;
+      v[g * 4 + 2] = __uint_as_float(r[g * 4 + 2]) + q.z;
+      v[g * 4 + 3] = __uint_as_float(r[g * 4 + 3]) + q.w;
+    }
+    epilogue_store<EPI>(p, row, col_base + c * 32, v);
   }
 }
 
@@ -1045,8 +1099,21 @@ __global__ void __launch_bounds__(192, 1)
             if (col_base + c < p.N) prefetch_l2(seg + c);
         }
       }
+      if (p.pf_partials && contrib > 1 && seg_end == it_end && i > tile_first) {
+        // the final piece of a split tile: its other contributors' partials were
+        // stored early (they own the tile's head) and may have left L2 under the
+        // weight stream; pull them back while this piece's MMAs run
+        const size_t slot_elems = static_cast<size_t>(BN / 32) * 128 * 32;
+        const float* ws0 = p.ws + static_cast<size_t>(tile) * p.slots * slot_elems;
+        for (int a = 0; a < contrib - 1; ++a)
+          for (size_t e = static_cast<size_t>(tid_e) * 32; e < slot_elems; e += 128 * 32)
+            prefetch_l2(ws0 + a * slot_elems + e);
+      }
       if (p.wait_mode == 2) mbar_wait_sleep(&tfull[acc], acc_phase); else if (p.wait_mode) mbar_wait_lane0(&tfull[acc], acc_phase); else mbar_wait(&tfull[acc], acc_phase);
-      if (ep_leader) gemm_stamp(p, 5, (i - it_begin) / kbs);
+      if (ep_leader) {
+        gemm_stamp(p, 5, (i - it_begin) / kbs);
+        if (seg_end == it_end) gemm_cta_stamp(p, 5);
+      }
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((quarter * 32) << 16) + acc * 256;
       auto release_tmem = [&]() {
@@ -1054,7 +1121,47 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_leader(&tempty[acc]);
       };
-      if (contrib == 1) {
+      // The CTA's last tile (the shared-memory ring is idle once its MMAs are done):
+      // stage the bf16 tile in shared memory and write whole rows (512 B per warp
+      // instruction) instead of 16 B per thread across 32 rows.
+      constexpr bool kStageable = EPI == EPI_BF16 || EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_RELU;
+      constexpr int ROWB = BN * 2 + 16;
+      auto stage_and_store = [&](auto&& chunk_values) {
+        uint8_t* stg = smem;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          chunk_values(c, v);
+          epilogue_math<EPI>(p, col_base + c * 32, v);
+          uint4* dst = reinterpret_cast<uint4*>(stg + row_in_tile * ROWB + c * 64);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            dst[g] = make_uint4(pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]), pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]),
+                                pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]), pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]));
+        }
+        release_tmem();
+        named_bar_sync(1, 128);
+        __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C);
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+          const int rr = static_cast<int>(quarter) * 32 + r;
+          const int grow = m_idx * BM + rr;
+          const int col = col_base + static_cast<int>(lane) * 8;
+          if (grow < p.M && static_cast<int>(lane) < BN / 8 && col < p.N)
+            *reinterpret_cast<uint4*>(C + static_cast<size_t>(grow) * p.N + col) =
+                *reinterpret_cast<const uint4*>(stg + rr * ROWB + lane * 16);
+        }
+      };
+      const bool staged = kStageable && p.stage_epi && seg_end == it_end;
+      if (contrib == 1 && staged) {
+        stage_and_store([&](int c, float (&v)[32]) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        });
+      } else if (contrib == 1) {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
@@ -1092,12 +1199,34 @@ __global__ void __launch_bounds__(192, 1)
             for (int a = 0; a < contrib - 1; ++a)
               while (ld_acquire(flags + a) == 0) {
               }
+            if (seg_end == it_end) gemm_cta_stamp(p, 6);
           }
           named_bar_sync(1, 128);
           __threadfence();
-          fixup_epilogue<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems, contrib - 1,
-                                       tid_e);
-          release_tmem();
+          if (staged) {
+            stage_and_store([&](int c, float (&v)[32]) {
+              float4 q[8];
+              partial_load(tile_ws, slot_elems, contrib - 1, c, tid_e, q);
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(t_row + c * 32, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                v[g * 4] = __uint_as_float(r[g * 4]) + q[g].x;
+                v[g * 4 + 1] = __uint_as_float(r[g * 4 + 1]) + q[g].y;
+                v[g * 4 + 2] = __uint_as_float(r[g * 4 + 2]) + q[g].z;
+                v[g * 4 + 3] = __uint_as_float(r[g * 4 + 3]) + q[g].w;
+              }
+            });
+          } else {
+            if (p.fix_depth >= 2)
+              fixup_epilogue_deep<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems,
+                                                contrib - 1, tid_e);
+            else
+              fixup_epilogue<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems,
+                                           contrib - 1, tid_e);
+            release_tmem();
+          }
           named_bar_sync(1, 128);
           if (ep_leader) {
             for (int a = 0; a < contrib - 1; ++a) flags[a] = 0;
@@ -1150,6 +1279,9 @@ struct GemmEnv {
   int pf = -1;                      // TK_GEMM_PF: weight prefetch distance (k-blocks)
   int exp = 0;                      // TK_GEMM_EXP: pipeline experiments (wrong results)
   int wait_mode = -1;               // TK_GEMM_WAIT
+  int fix_depth = -1;               // TK_GEMM_FIXDEPTH
+  int stage_epi = -1;               // TK_GEMM_STAGE_EPI
+  int pf_partials = -1;             // TK_GEMM_PFPART
   GemmEnv() {
     no_skinny = getenv("TK_NO_SKINNY") != nullptr;
     no_pair = getenv("TK_NO_PAIR") != nullptr;
@@ -1160,6 +1292,9 @@ struct GemmEnv {
     if (const char* f = getenv("TK_GEMM_PF")) pf = atoi(f);
     if (const char* f = getenv("TK_GEMM_EXP")) exp = atoi(f);
     if (const char* f = getenv("TK_GEMM_WAIT")) wait_mode = atoi(f);
+    if (const char* f = getenv("TK_GEMM_FIXDEPTH")) fix_depth = atoi(f);
+    if (const char* f = getenv("TK_GEMM_STAGE_EPI")) stage_epi = atoi(f);
+    if (const char* f = getenv("TK_GEMM_PFPART")) pf_partials = atoi(f);
     if (const char* c = getenv("TK_GEMM_MAX_CTAS")) max_ctas = atoi(c);
   }
   int max_ctas = 0;  // TK_GEMM_MAX_CTAS: cap the CTAs (skips the split-minimising pick)
@@ -1692,6 +1827,9 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   a.pf_dist = genv().pf >= 0 ? genv().pf : 0;
   a.exp = genv().exp;
   a.wait_mode = genv().wait_mode >= 0 ? genv().wait_mode : 0;
+  a.fix_depth = genv().fix_depth >= 0 ? genv().fix_depth : 1;
+  a.stage_epi = genv().stage_epi >= 0 ? genv().stage_epi : 1;
+  a.pf_partials = genv().pf_partials >= 0 ? genv().pf_partials : 0;
   a.slots = pl.slots;
   a.total_iters = pl.total_iters;
   const int64_t tiles = static_cast<int64_t>(a.tiles_m) * a.tiles_n;

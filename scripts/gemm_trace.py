@@ -71,12 +71,12 @@ def main():
            "first_full_after_start": get(1, 0) - base,
            "total_cycles": get(2, n - 1) - base, "epilogue_seen_at": tiles}
     print(json.dumps(res))
-    cta = (ctypes.c_uint64 * (5 * 256))()
-    native.check(native.load().tk_debug_gemm_cta_trace(cta, 5 * 256), "cta trace")
+    cta = (ctypes.c_uint64 * (7 * 256))()
+    native.check(native.load().tk_debug_gemm_cta_trace(cta, 7 * 256), "cta trace")
     n_cta = sum(1 for c in range(256) if cta[c])
     t0 = min(cta[c] for c in range(n_cta))
     rel = lambda k: [(cta[k * 256 + c] - t0) / 1e3 if cta[k * 256 + c] else None for c in range(n_cta)]  # noqa: E731
-    ent, first, last, epi, ext = (rel(k) for k in range(5))
+    ent, first, last, epi, ext, saw, ready = (rel(k) for k in range(7))
     lead = [c for c in range(n_cta) if first[c] is not None]
     summ = lambda v: (round(min(v), 2), round(sorted(v)[len(v) // 2], 2), round(max(v), 2))  # noqa: E731
     print(json.dumps({"ctas": n_cta, "entry_us(min,med,max)": summ([x for x in ent if x is not None]),
@@ -85,6 +85,12 @@ def main():
                       "epilogue_done_us": summ([x for x in epi if x is not None]),
                       "exit_us": summ([x for x in ext if x is not None]),
                       "mainloop_us": summ([last[c] - first[c] for c in lead])}))
+    fx = [c for c in range(n_cta) if ready[c] is not None and saw[c] is not None]
+    if fx:
+        print(json.dumps({"fixup_ctas": len(fx),
+                          "saw_last_acc_after_commit_us": summ([saw[c] - last[c - c % 2] for c in fx if last[c - c % 2] is not None]),
+                          "partials_ready_wait_us": summ([ready[c] - saw[c] for c in fx]),
+                          "fixup_work_us": summ([epi[c] - ready[c] for c in fx if epi[c] is not None])}))
     S = args.stages
     lat = [(get(4, j + S) - get(2, j), get(1, j + S) - get(4, j + S), get(0, j + S) - get(4, j + S))
            for j in range(lo, min(hi, n - S)) if get(4, j + S)]
