@@ -40,11 +40,21 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > built for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, experiments: bool = False) -> Path:
+    """experiments=True (or TK_BUILD_EXPERIMENTS=1) builds lib/libtetri_exp.so with the
+    GEMM experiment hooks (TK_GEMM_TRACE / _EXP / _WAIT / _PF ...); scripts load it via
+    TK_LIB.  The product library never contains them."""
+    experiments = experiments or bool(os.environ.get("TK_BUILD_EXPERIMENTS"))
+    if experiments:
+        return _build_into(LIB_DIR / "libtetri_exp.so", LIB_DIR / "obj_exp", ["-DTK_GEMM_EXPERIMENTS"],
+                           verbose)
     if not force and not _stale():
         return LIB
+    return _build_into(LIB, LIB_DIR / "obj", [], verbose)
+
+
+def _build_into(LIB: Path, obj_dir: Path, extra: list, verbose: bool) -> Path:
     LIB_DIR.mkdir(exist_ok=True)
-    obj_dir = LIB_DIR / "obj"
     obj_dir.mkdir(exist_ok=True)
     nvcc = _nvcc()
     objs = []
@@ -52,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for src in SOURCES:
         obj = obj_dir / (Path(src).stem + ".o")
         objs.append(obj)
-        cmd = [nvcc, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc, *ARCH, *FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -76,13 +76,25 @@ struct GemmArgs {
   QkvScatter kv;  // EPI_QKV_PAGED only
 };
 
+// Experiment hooks (pipeline stamps, load/MMA ablations, alternative waits) exist
+// only in builds with TK_GEMM_EXPERIMENTS (TK_BUILD_EXPERIMENTS=1 python -m
+// paper_2401_11181_b200.build): the runtime checks alone cost the production
+// kernel ~12% (measured), so they are compiled out.
+#ifdef TK_GEMM_EXPERIMENTS
+constexpr bool kGemmExp = true;
+#else
+constexpr bool kGemmExp = false;
+#endif
+
 // Pipeline stamps of CTA 0 (experiments; scripts/gemm_trace.py): kind x k-block.
 //   0 issuer before full-wait, 1 after it, 2 after the k-block's MMAs + commit,
 //   3 producer before empty-wait, 4 after it, 5 epilogue saw the accumulator (per tile)
 constexpr int kGemmTraceN = 1024;
 __device__ unsigned long long g_gemm_trace[6 * kGemmTraceN];
 __device__ __forceinline__ void gemm_stamp(const GemmArgs& p, int kind, long long j) {
-  if (p.trace && blockIdx.x == 0 && j < kGemmTraceN) g_gemm_trace[kind * kGemmTraceN + j] = clock64();
+  if constexpr (kGemmExp) {
+    if (p.trace && blockIdx.x == 0 && j < kGemmTraceN) g_gemm_trace[kind * kGemmTraceN + j] = clock64();
+  }
 }
 
 // Per-CTA globaltimer stamps (ns): 0 entry, 1 issuer saw the first stage, 2 last
@@ -95,7 +107,9 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 __device__ __forceinline__ void gemm_cta_stamp(const GemmArgs& p, int kind) {
-  if (p.trace && blockIdx.x < 256) g_gemm_cta[kind * 256 + blockIdx.x] = globaltimer_ns();
+  if constexpr (kGemmExp) {
+    if (p.trace && blockIdx.x < 256) g_gemm_cta[kind * 256 + blockIdx.x] = globaltimer_ns();
+  }
 }
 
 int gemm_debug_cta_trace(unsigned long long* host, int n) {
@@ -953,15 +967,17 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t pol_b = p.b_pol == 0   ? l2_policy_evict_first()
                              : p.b_pol == 1 ? l2_policy_evict_normal()
                                             : l2_policy_evict_last();
-      const int xbytes = p.exp == 2 ? 2 * A_BYTES : p.exp == 3 ? PAIR_STAGE_BYTES - 2 * A_BYTES
-                                                                : PAIR_STAGE_BYTES;
+      const int xbytes = !kGemmExp ? PAIR_STAGE_BYTES
+                         : p.exp == 2 ? 2 * A_BYTES
+                         : p.exp == 3 ? PAIR_STAGE_BYTES - 2 * A_BYTES
+                                      : PAIR_STAGE_BYTES;
       auto load_a = [&](int ctile, int kb, int stage) {
-        if (p.exp == 3) return;
+        if (kGemmExp && p.exp == 3) return;
         const int m_idx = (ctile % groups_m) * CS + rank;  // this CTA's 128-row tile
         tma_load_2d_pair(sa + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, m_idx * BM, pol_a);
       };
       auto load_b = [&](int ctile, int kb, int stage) {
-        if (p.exp == 2) return;
+        if (kGemmExp && p.exp == 2) return;
         const int n_idx = ctile / groups_m;
         const int brow = n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS;
         uint8_t* bdst = sb + stage * BH_BYTES + pair * SLICE_BYTES;
@@ -994,7 +1010,7 @@ __global__ void __launch_bounds__(192, 1)
       pf_tile = ctile;
       pf_kb = kb;
       pf_i = it_begin + pre;
-      if (pf_dist > 0) prefetch_b_upto(it_begin + pre + pf_dist);
+      if (kGemmExp && pf_dist > 0) prefetch_b_upto(it_begin + pre + pf_dist);
       griddep_wait();
       ctile = tile0;
       kb = kb0;
@@ -1005,7 +1021,7 @@ __global__ void __launch_bounds__(192, 1)
       int stage = pre % STAGES;
       uint32_t phase = pre == STAGES ? 1u : 0u;
       for (long long i = it_begin + pre; i < it_end; ++i) {
-        if (pf_dist > 0) prefetch_b_upto(i + pf_dist + 1);
+        if (kGemmExp && pf_dist > 0) prefetch_b_upto(i + pf_dist + 1);
         gemm_stamp(p, 3, i - it_begin);
         mbar_wait(&empty[stage], phase ^ 1);
         gemm_stamp(p, 4, i - it_begin);
@@ -1035,12 +1051,12 @@ __global__ void __launch_bounds__(192, 1)
         const int ctile = static_cast<int>(i / kbs);
         const long long seg_end = min(it_end, static_cast<long long>(ctile + 1) * kbs);
         const int nkb = static_cast<int>(seg_end - i);
-        if (p.wait_mode) mbar_wait_lane0(&tempty[acc], acc_phase ^ 1); else mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (kGemmExp && p.wait_mode) mbar_wait_lane0(&tempty[acc], acc_phase ^ 1); else mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
         for (int k = 0; k < nkb; ++k) {
           if (lane == 0) gemm_stamp(p, 0, i - it_begin + k);
-          if (p.wait_mode) mbar_wait_lane0(&full[stage], phase); else mbar_wait(&full[stage], phase);
+          if (kGemmExp && p.wait_mode) mbar_wait_lane0(&full[stage], phase); else mbar_wait(&full[stage], phase);
           if (lane == 0) {
             gemm_stamp(p, 1, i - it_begin + k);
             if (i - it_begin + k == 0) gemm_cta_stamp(p, 1);
@@ -1049,7 +1065,7 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t a_desc = umma_desc_sw128(sa_base + stage * A_BYTES);
           const uint64_t b_desc = umma_desc_sw128(sb_base + stage * BH_BYTES);
           if (elect_one_sync()) {
-            if (p.exp != 1) {
+            if (!kGemmExp || p.exp != 1) {
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk)  // +32 B per K step = +2 descriptor units
                 umma_bf16_pair(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
@@ -1099,7 +1115,7 @@ __global__ void __launch_bounds__(192, 1)
             if (col_base + c < p.N) prefetch_l2(seg + c);
         }
       }
-      if (p.pf_partials && contrib > 1 && seg_end == it_end && i > tile_first) {
+      if (kGemmExp && p.pf_partials && contrib > 1 && seg_end == it_end && i > tile_first) {
         // the final piece of a split tile: its other contributors' partials were
         // stored early (they own the tile's head) and may have left L2 under the
         // weight stream; pull them back while this piece's MMAs run
@@ -1109,7 +1125,9 @@ __global__ void __launch_bounds__(192, 1)
           for (size_t e = static_cast<size_t>(tid_e) * 32; e < slot_elems; e += 128 * 32)
             prefetch_l2(ws0 + a * slot_elems + e);
       }
-      if (p.wait_mode == 2) mbar_wait_sleep(&tfull[acc], acc_phase); else if (p.wait_mode) mbar_wait_lane0(&tfull[acc], acc_phase); else mbar_wait(&tfull[acc], acc_phase);
+      if (kGemmExp && p.wait_mode == 2) mbar_wait_sleep(&tfull[acc], acc_phase);
+      else if (kGemmExp && p.wait_mode) mbar_wait_lane0(&tfull[acc], acc_phase);
+      else mbar_wait(&tfull[acc], acc_phase);
       if (ep_leader) {
         gemm_stamp(p, 5, (i - it_begin) / kbs);
         if (seg_end == it_end) gemm_cta_stamp(p, 5);
@@ -1219,7 +1237,7 @@ __global__ void __launch_bounds__(192, 1)
               }
             });
           } else {
-            if (p.fix_depth >= 2)
+            if (kGemmExp && p.fix_depth >= 2)
               fixup_epilogue_deep<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems,
                                                 contrib - 1, tid_e);
             else

@@ -10,6 +10,7 @@ capacity break, as pdsim/decode.py:63-66), everything else -> NativeError.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -106,7 +107,7 @@ def load(path: str | Path | None = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ["TK_LIB"]) if os.environ.get("TK_LIB") else LIB_PATH
     if not p.exists():
         raise NativeError(f"{p} not built; run `python -m paper_2401_11181_b200.build`")
     lib = C.CDLL(str(p))

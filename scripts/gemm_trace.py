@@ -16,6 +16,9 @@ import sys
 from pathlib import Path
 
 os.environ["TK_GEMM_TRACE"] = "1"
+# the hooks exist only in the experiments build (lib/libtetri_exp.so)
+os.environ.setdefault("TK_LIB", str(Path(__file__).resolve().parents[1] /
+                                    "paper_2401_11181_b200" / "lib" / "libtetri_exp.so"))
 import torch  # noqa: E402
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
