@@ -918,6 +918,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* fix_bar = reinterpret_cast<uint64_t*>(last_flag + 1);  // final fixup's bulk load
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) gemm_cta_stamp(p, 0);
@@ -936,6 +937,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 8);  // leader: 4 epilogue warps x 2 CTAs
     }
+    mbar_init(fix_bar, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
@@ -1221,7 +1223,45 @@ __global__ void __launch_bounds__(192, 1)
           }
           named_bar_sync(1, 128);
           __threadfence();
-          if (staged) {
+          // Final fixup of the CTA: one bulk copy brings every partial slot into the
+          // idle ring behind the staging tile (one round trip instead of one per
+          // 32-column chunk, which left ~7 us on the critical path).
+          const int nsl = contrib - 1;
+          constexpr int kStageArea = (128 * ROWB + 1023) & ~1023;
+          const bool bulk = staged && kStageArea + nsl * static_cast<int>(slot_elems) * 4 <=
+                                          STAGES * STAGE_BYTES;
+          if (bulk) {
+            float* pbuf = reinterpret_cast<float*>(smem + kStageArea);
+            if (ep_leader) {
+              fence_proxy_async_global();
+              const uint32_t slot_bytes = static_cast<uint32_t>(slot_elems) * 4;
+              mbar_expect_tx(fix_bar, nsl * slot_bytes);
+              for (int a = 0; a < nsl; ++a)
+                for (uint32_t off = 0; off < slot_bytes; off += 32768)
+                  bulk_g2s(reinterpret_cast<uint8_t*>(pbuf + a * slot_elems) + off,
+                           reinterpret_cast<const uint8_t*>(tile_ws + a * slot_elems) + off,
+                           slot_bytes - off < 32768 ? slot_bytes - off : 32768, fix_bar);
+            }
+            mbar_wait(fix_bar, 0);
+            const float4* p4 = reinterpret_cast<const float4*>(pbuf);
+            stage_and_store([&](int c, float (&v)[32]) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(t_row + c * 32, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                float4 q = p4[(c * 8 + g) * 128 + tid_e];
+                for (int a = 1; a < nsl; ++a) {
+                  const float4 t = p4[a * (slot_elems / 4) + (c * 8 + g) * 128 + tid_e];
+                  q.x += t.x; q.y += t.y; q.z += t.z; q.w += t.w;
+                }
+                v[g * 4] = __uint_as_float(r[g * 4]) + q.x;
+                v[g * 4 + 1] = __uint_as_float(r[g * 4 + 1]) + q.y;
+                v[g * 4 + 2] = __uint_as_float(r[g * 4 + 2]) + q.z;
+                v[g * 4 + 3] = __uint_as_float(r[g * 4 + 3]) + q.w;
+              }
+            });
+          } else if (staged) {
             stage_and_store([&](int c, float (&v)[32]) {
               float4 q[8];
               partial_load(tile_ws, slot_elems, contrib - 1, c, tid_e, q);

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--m", type=int, nargs="*", default=[512])
     ap.add_argument("--shapes", nargs="*", default=list(SHAPES))
+    ap.add_argument("--nk", nargs="*", default=[],
+                    help="extra N,K shapes (bf16+bias epilogue), e.g. 5120,2560")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--cublas", action="store_true",
                     help="time torch.matmul (cuBLAS) on the same shapes instead, for reference")
@@ -35,6 +37,10 @@ def main():
     ap.add_argument("--chain", type=int, default=0,
                     help="time N back-to-back layers of all --shapes (decode-style weight streaming)")
     args = ap.parse_args()
+    for nk in args.nk:
+        n_, k_ = (int(x) for x in nk.split(","))
+        SHAPES[nk] = (n_, k_, native.EPI_BF16_BIAS)
+        args.shapes.append(nk)
     native.load()
     if args.chain:
         return chain(args)
