@@ -25,6 +25,10 @@ WANT = {
     "launch__grid_size": "grid",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
     "smsp__inst_executed.sum": "inst",
+    # tcgen05 (UMMA) activity; the legacy tensor-pipe counters above stay near zero
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tcgen05_active_pct_of_active",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tcgen05_active_pct_of_elapsed",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock",
 }
 
 
