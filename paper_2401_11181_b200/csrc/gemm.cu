@@ -883,29 +883,32 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
 // BN (tile width) is 256 (stream-K), or 160 for a one-wave data-parallel
 // schedule: O-proj at M=512 as 32 clusters of 512x160 (no split tile); 256-
 // wide tiles would leave SMs idle or need a split-K exchange per tile.
-template <int BN>
+// KS = 64-wide k-blocks per ring stage (one barrier round trip per KS blocks).
+template <int BN, int KS = 1>
 struct PairCfg {
-  static constexpr int A_BYTES = 128 * 64 * 2;
-  static constexpr int BH_BYTES = (BN / 2) * 64 * 2;
+  static constexpr int A_BYTES = 128 * 64 * 2 * KS;
+  static constexpr int BH_BYTES = (BN / 2) * 64 * 2 * KS;
   static constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
   static constexpr int STAGES = (232448 - 2048) / STAGE_BYTES > 8 ? 8 : (232448 - 2048) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 256 + 1024;
 };
 
-template <int EPI, int CS, int BN>
+template <int EPI, int CS, int BN, int KS>
 __global__ void __launch_bounds__(192, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b, const GemmArgs p) {
   constexpr int BM = 128, BK = 64;
   static_assert(BN % 32 == 0 && BN <= 256 && (BN / 2 / (CS / 2)) % 8 == 0, "pair tile width");
-  constexpr int STAGES = PairCfg<BN>::STAGES;
-  constexpr int A_BYTES = BM * BK * 2;        // own 128 rows
-  constexpr int BH_BYTES = (BN / 2) * BK * 2;  // own half of the B tile
+  constexpr int STAGES = PairCfg<BN, KS>::STAGES;
+  constexpr int A_BOX = BM * BK * 2;          // own 128 rows of one 64-wide k-block
+  constexpr int BH_BOX = (BN / 2) * BK * 2;   // own half of the B tile, one k-block
+  constexpr int A_BYTES = KS * A_BOX;         // per stage (KS k-blocks)
+  constexpr int BH_BYTES = KS * BH_BOX;
   constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
   constexpr int PAIR_STAGE_BYTES = 2 * STAGE_BYTES;
   constexpr int NPAIRS = CS / 2;
   constexpr int SLICE_ROWS = (BN / 2) / NPAIRS;  // B-half rows each CTA loads
-  constexpr int SLICE_BYTES = SLICE_ROWS * BK * 2;
+  constexpr int SLICE_BYTES = SLICE_ROWS * BK * 2;  // per k-block box
   constexpr int TMEM_COLS = 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -976,17 +979,24 @@ __global__ void __launch_bounds__(192, 1)
       auto load_a = [&](int ctile, int kb, int stage) {
         if (kGemmExp && p.exp == 3) return;
         const int m_idx = (ctile % groups_m) * CS + rank;  // this CTA's 128-row tile
-        tma_load_2d_pair(sa + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, m_idx * BM, pol_a);
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+          tma_load_2d_pair(sa + stage * A_BYTES + s * A_BOX, &tmap_a, &full[stage],
+                           (kb * KS + s) * BK, m_idx * BM, pol_a);
       };
       auto load_b = [&](int ctile, int kb, int stage) {
         if (kGemmExp && p.exp == 2) return;
         const int n_idx = ctile / groups_m;
         const int brow = n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS;
-        uint8_t* bdst = sb + stage * BH_BYTES + pair * SLICE_BYTES;
-        if constexpr (CS == 2)
-          tma_load_2d_pair(bdst, &tmap_b, &full[stage], kb * BK, brow, pol_b);
-        else
-          tma_load_2d_pair_mc(bdst, &tmap_b, &full[stage], kb * BK, brow, half_mask, pol_b);
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          uint8_t* bdst = sb + stage * BH_BYTES + s * BH_BOX + pair * SLICE_BYTES;
+          if constexpr (CS == 2)
+            tma_load_2d_pair(bdst, &tmap_b, &full[stage], (kb * KS + s) * BK, brow, pol_b);
+          else
+            tma_load_2d_pair_mc(bdst, &tmap_b, &full[stage], (kb * KS + s) * BK, brow, half_mask,
+                                pol_b);
+        }
       };
       // optional L2 prefetch of this CTA's weight slice ahead of the ring (TK_GEMM_PF;
       // measured slower, off by default)
@@ -996,7 +1006,7 @@ __global__ void __launch_bounds__(192, 1)
       auto prefetch_b_upto = [&](long long upto) {
         for (; pf_i < upto && pf_i < it_end; ++pf_i) {
           const int n_idx = pf_tile / groups_m;
-          tma_prefetch_2d(&tmap_b, pf_kb * BK, n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS);
+          tma_prefetch_2d(&tmap_b, pf_kb * KS * BK, n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS);
           if (++pf_kb == kbs) { pf_kb = 0; ++pf_tile; }
         }
       };
@@ -1064,14 +1074,17 @@ __global__ void __launch_bounds__(192, 1)
             if (i - it_begin + k == 0) gemm_cta_stamp(p, 1);
           }
           tc_fence_after();
-          const uint64_t a_desc = umma_desc_sw128(sa_base + stage * A_BYTES);
-          const uint64_t b_desc = umma_desc_sw128(sb_base + stage * BH_BYTES);
           if (elect_one_sync()) {
             if (!kGemmExp || p.exp != 1) {
 #pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk)  // +32 B per K step = +2 descriptor units
-                umma_bf16_pair(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
-                               (k > 0 || kk > 0) ? 1u : 0u);
+              for (int s = 0; s < KS; ++s) {
+                const uint64_t a_desc = umma_desc_sw128(sa_base + stage * A_BYTES + s * A_BOX);
+                const uint64_t b_desc = umma_desc_sw128(sb_base + stage * BH_BYTES + s * BH_BOX);
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)  // +32 B per K step = +2 descriptor units
+                  umma_bf16_pair(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
+                                 (k > 0 || s > 0 || kk > 0) ? 1u : 0u);
+              }
             }
             umma_commit_pair_mc(&empty[stage], all_mask);
             gemm_stamp(p, 2, i - it_begin + k);
@@ -1339,6 +1352,7 @@ struct GemmEnv {
   int wait_mode = -1;               // TK_GEMM_WAIT
   int fix_depth = -1;               // TK_GEMM_FIXDEPTH
   int stage_epi = -1;               // TK_GEMM_STAGE_EPI
+  int ks = -1;                      // TK_GEMM_KS: k-blocks per ring stage of 160-wide tiles
   int pf_partials = -1;             // TK_GEMM_PFPART
   GemmEnv() {
     no_skinny = getenv("TK_NO_SKINNY") != nullptr;
@@ -1352,6 +1366,7 @@ struct GemmEnv {
     if (const char* f = getenv("TK_GEMM_WAIT")) wait_mode = atoi(f);
     if (const char* f = getenv("TK_GEMM_FIXDEPTH")) fix_depth = atoi(f);
     if (const char* f = getenv("TK_GEMM_STAGE_EPI")) stage_epi = atoi(f);
+    if (const char* f = getenv("TK_GEMM_KS")) ks = atoi(f);
     if (const char* f = getenv("TK_GEMM_PFPART")) pf_partials = atoi(f);
     if (const char* c = getenv("TK_GEMM_MAX_CTAS")) max_ctas = atoi(c);
   }
@@ -1457,6 +1472,7 @@ struct GemmPlan {
   bool skinny;  // swap-AB weight-streaming path (M <= 128)
   int nb;       // skinny: UMMA N (batch rows, padded)
   int bn, cs, tiles_m, tiles_n, kbs, clusters, slots;
+  int ks;  // pair kernel: 64-wide k-blocks per ring stage (kbs counts stages)
   long long total_iters;
   int64_t ws_bytes;
 };
@@ -1552,6 +1568,13 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
     }
   }
   pl.tiles_n = (N + pl.bn - 1) / pl.bn;
+  pl.ks = 1;
+  // 160-wide tiles: two k-blocks per ring stage (O-proj at M=512: 34.8 -> 32.8 us,
+  // the per-launch fill cost halves); TK_GEMM_KS=1 restores one
+  if (pl.pair && pl.bn == 160 && pl.kbs % 2 == 0 && genv().ks != 1) {
+    pl.ks = 2;
+    pl.kbs /= 2;
+  }
   pl.total_iters = static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
   clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, pl.total_iters / 4)));
   // Long K (FC2: 320 k-blocks per tile) amortises a split tile's exchange: use
@@ -1628,20 +1651,20 @@ static int skinny_epi(const CUtensorMap& tw, const CUtensorMap& tx, const GemmAr
   return TK_EINVAL;
 }
 
-template <int EPI, int CS, int BN>
-static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
-                       int clusters, cudaStream_t stream) {
-  auto kern = gemm_pair_kernel<EPI, CS, BN>;
+template <int EPI, int CS, int BN, int KS>
+static int launch_pair_ks(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                          int clusters, cudaStream_t stream) {
+  auto kern = gemm_pair_kernel<EPI, CS, BN, KS>;
   static bool configured = false;
   if (!configured) {
     TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 PairCfg<BN>::SMEM));
+                                 PairCfg<BN, KS>::SMEM));
     configured = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * CS);
   cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = PairCfg<BN>::SMEM;
+  cfg.dynamicSmemBytes = PairCfg<BN, KS>::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1655,16 +1678,24 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   return TK_OK;
 }
 
+// a.kbs counts stages of KS k-blocks
+template <int EPI, int CS, int BN>
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                       int clusters, cudaStream_t stream, int ks) {
+  if (ks == 2) return launch_pair_ks<EPI, CS, BN, 2>(ta, tb, a, clusters, stream);
+  return launch_pair_ks<EPI, CS, BN, 1>(ta, tb, a, clusters, stream);
+}
+
 template <int CS, int BN>
 static int pair_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int clusters,
-                    cudaStream_t s) {
+                    cudaStream_t s, int ks = 1) {
   switch (a.epi) {
-    case EPI_BF16: return launch_pair<EPI_BF16, CS, BN>(ta, tb, a, clusters, s);
-    case EPI_BF16_BIAS: return launch_pair<EPI_BF16_BIAS, CS, BN>(ta, tb, a, clusters, s);
-    case EPI_BF16_BIAS_RELU: return launch_pair<EPI_BF16_BIAS_RELU, CS, BN>(ta, tb, a, clusters, s);
-    case EPI_F32_BIAS_RESID: return launch_pair<EPI_F32_BIAS_RESID, CS, BN>(ta, tb, a, clusters, s);
-    case EPI_F32: return launch_pair<EPI_F32, CS, BN>(ta, tb, a, clusters, s);
-    case EPI_QKV_PAGED: return launch_pair<EPI_QKV_PAGED, CS, BN>(ta, tb, a, clusters, s);
+    case EPI_BF16: return launch_pair<EPI_BF16, CS, BN>(ta, tb, a, clusters, s, ks);
+    case EPI_BF16_BIAS: return launch_pair<EPI_BF16_BIAS, CS, BN>(ta, tb, a, clusters, s, ks);
+    case EPI_BF16_BIAS_RELU: return launch_pair<EPI_BF16_BIAS_RELU, CS, BN>(ta, tb, a, clusters, s, ks);
+    case EPI_F32_BIAS_RESID: return launch_pair<EPI_F32_BIAS_RESID, CS, BN>(ta, tb, a, clusters, s, ks);
+    case EPI_F32: return launch_pair<EPI_F32, CS, BN>(ta, tb, a, clusters, s, ks);
+    case EPI_QKV_PAGED: return launch_pair<EPI_QKV_PAGED, CS, BN>(ta, tb, a, clusters, s, ks);
   }
   set_error("unknown gemm epilogue");
   return TK_EINVAL;
@@ -1672,7 +1703,7 @@ static int pair_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs
 
 template <int CS>
 static int query_pair_clusters() {
-  auto kern = gemm_pair_kernel<EPI_BF16, CS, 256>;
+  auto kern = gemm_pair_kernel<EPI_BF16, CS, 256, 1>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256>::SMEM) !=
       cudaSuccess) {
     cudaGetLastError();
@@ -1901,8 +1932,8 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
     rc = make_tmap_kmajor(&tb, B, N, K, pl.bn / 2 / (pl.cs / 2));
     if (rc) return rc;
     if (pl.bn == 160) {
-      if (pl.cs == 4) return pair_epi<4, 160>(ta, tb, a, pl.clusters, stream);
-      return pair_epi<2, 160>(ta, tb, a, pl.clusters, stream);
+      if (pl.cs == 4) return pair_epi<4, 160>(ta, tb, a, pl.clusters, stream, pl.ks);
+      return pair_epi<2, 160>(ta, tb, a, pl.clusters, stream, pl.ks);
     }
     if (pl.cs == 4) return pair_epi<4, 256>(ta, tb, a, pl.clusters, stream);
     return pair_epi<2, 256>(ta, tb, a, pl.clusters, stream);
