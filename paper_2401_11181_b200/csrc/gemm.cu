@@ -1571,7 +1571,8 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
   pl.ks = 1;
   // 160-wide tiles: two k-blocks per ring stage (O-proj at M=512: 34.8 -> 32.8 us,
   // the per-launch fill cost halves); TK_GEMM_KS=1 restores one
-  if (pl.pair && pl.bn == 160 && pl.kbs % 2 == 0 && genv().ks != 1) {
+  if (pl.pair && pl.kbs % 2 == 0 &&
+      ((pl.bn == 160 && genv().ks != 1) || (pl.bn == 256 && genv().ks == 4))) {
     pl.ks = 2;
     pl.kbs /= 2;
   }
@@ -1935,8 +1936,8 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
       if (pl.cs == 4) return pair_epi<4, 160>(ta, tb, a, pl.clusters, stream, pl.ks);
       return pair_epi<2, 160>(ta, tb, a, pl.clusters, stream, pl.ks);
     }
-    if (pl.cs == 4) return pair_epi<4, 256>(ta, tb, a, pl.clusters, stream);
-    return pair_epi<2, 256>(ta, tb, a, pl.clusters, stream);
+    if (pl.cs == 4) return pair_epi<4, 256>(ta, tb, a, pl.clusters, stream, pl.ks);
+    return pair_epi<2, 256>(ta, tb, a, pl.clusters, stream, pl.ks);
   }
   if (pl.bn == 256) return dispatch_cs<256>(B, N, K, ta, a, pl.clusters, stream);
   return dispatch_cs<128>(B, N, K, ta, a, pl.clusters, stream);
