@@ -58,12 +58,14 @@ constexpr int kBarBytes = 256;
 constexpr int kSmem = 2 * kQTile + kRing * kEntry + kBarBytes + 1024;
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
-constexpr int kPartStride = kD + 4;       // partial row: O[128], m, l (16-byte aligned rows)
+// partial row (bytes): unnormalised O[128] as bf16 (relative precision is what bf16
+// keeps, magnitude-independent), then m, l as fp32; 16-byte aligned rows
+constexpr int kPartRowBytes = kD * 2 + 16;
 constexpr int kMinBlocksPerCta = 2;
 }  // namespace
 
 int64_t fa_partial_bytes() {
-  return static_cast<int64_t>(kFaMaxPieces) * 2 * kRows * kPartStride * 4;
+  return static_cast<int64_t>(kFaMaxPieces) * 2 * kRows * kPartRowBytes;
 }
 
 // ------------------------------------------------------------ fp32x2 helpers
@@ -391,11 +393,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kv_end_t = t ? v.kv_end[1] : v.kv_end[0];
       if (n_t == 0) {
         if (v.piece >= 0 && nrows > 0) {  // nothing visible in this piece: empty partial
-          float* dst = p.partial + ((static_cast<size_t>(v.piece) * 2 + t) * kRows + r) * kPartStride;
-          for (int c = 0; c < kD; c += 4)
-            *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-          dst[kD] = -INFINITY;
-          dst[kD + 1] = 0.f;
+          uint8_t* dst = reinterpret_cast<uint8_t*>(p.partial) +
+                         ((static_cast<size_t>(v.piece) * 2 + t) * kRows + r) * kPartRowBytes;
+          for (int c = 0; c < kD * 2; c += 16)
+            *reinterpret_cast<uint4*>(dst + c) = make_uint4(0u, 0u, 0u, 0u);
+          reinterpret_cast<float*>(dst + kD * 2)[0] = -INFINITY;
+          reinterpret_cast<float*>(dst + kD * 2)[1] = 0.f;
         }
         continue;
       }
@@ -540,20 +543,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else {
-        float* dst = p.partial + ((static_cast<size_t>(v.piece) * 2 + t) * kRows + r) * kPartStride;
+        uint8_t* dst = reinterpret_cast<uint8_t*>(p.partial) +
+                       ((static_cast<size_t>(v.piece) * 2 + t) * kRows + r) * kPartRowBytes;
 #pragma unroll 1
         for (int c = 0; c < kD / 32; ++c) {
           uint32_t w[32];
           tmem_ld_32x32b_x32(t_o + c * 32, w);
           tmem_wait_ld();
 #pragma unroll
-          for (int g = 0; g < 8; ++g)
-            *reinterpret_cast<float4*>(dst + c * 32 + g * 4) =
-                make_float4(__uint_as_float(w[g * 4]), __uint_as_float(w[g * 4 + 1]),
-                            __uint_as_float(w[g * 4 + 2]), __uint_as_float(w[g * 4 + 3]));
+          for (int g = 0; g < 4; ++g) {
+            uint4 pk;
+            pk.x = pack_bf16x2(__uint_as_float(w[g * 8 + 0]), __uint_as_float(w[g * 8 + 1]));
+            pk.y = pack_bf16x2(__uint_as_float(w[g * 8 + 2]), __uint_as_float(w[g * 8 + 3]));
+            pk.z = pack_bf16x2(__uint_as_float(w[g * 8 + 4]), __uint_as_float(w[g * 8 + 5]));
+            pk.w = pack_bf16x2(__uint_as_float(w[g * 8 + 6]), __uint_as_float(w[g * 8 + 7]));
+            *reinterpret_cast<uint4*>(dst + c * 64 + g * 16) = pk;
+          }
         }
-        dst[kD] = m_used;
-        dst[kD + 1] = l;
+        reinterpret_cast<float*>(dst + kD * 2)[0] = m_used;
+        reinterpret_cast<float*>(dst + kD * 2)[1] = l;
       }
       tc_fence_before();
       __syncwarp();
@@ -582,7 +590,8 @@ __global__ void __launch_bounds__(256)
   const int r = rg * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= nrows) return;
   auto row_of = [&](int x) {
-    return partial + ((static_cast<size_t>(g.first_piece + x) * 2 + t) * kRows + r) * kPartStride;
+    return reinterpret_cast<const uint8_t*>(partial) +
+           ((static_cast<size_t>(g.first_piece + x) * 2 + t) * kRows + r) * kPartRowBytes;
   };
   float M = -INFINITY, L = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -592,10 +601,14 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (base + k < g.n_pieces) {
-        const float* src = row_of(base + k);
-        m[k] = __ldcg(src + kD);
-        l[k] = __ldcg(src + kD + 1);
-        v[k] = __ldcg(reinterpret_cast<const float4*>(src) + lane);
+        const uint8_t* src = row_of(base + k);
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(src + kD * 2));
+        m[k] = ml.x;
+        l[k] = ml.y;
+        const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(src) + lane);
+        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+        v[k] = make_float4(lo.x, lo.y, hi.x, hi.y);
       } else {
         m[k] = -INFINITY;
         l[k] = 0.f;
