@@ -898,7 +898,10 @@ __global__ void __launch_bounds__(192, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b, const GemmArgs p) {
   constexpr int BM = 128, BK = 64;
-  static_assert(BN % 32 == 0 && BN <= 256 && (BN / 2 / (CS / 2)) % 8 == 0, "pair tile width");
+  // BN % 32 != 0 (144): data-parallel one-tile-per-CTA schedules with a staged bf16
+  // epilogue only (the host guarantees it); the last 32-column chunk is half used
+  static_assert(BN % 16 == 0 && BN <= 256 && (BN / 2 / (CS / 2)) % 8 == 0, "pair tile width");
+  constexpr int NCH = (BN + 31) / 32;
   constexpr int STAGES = PairCfg<BN, KS>::STAGES;
   constexpr int A_BOX = BM * BK * 2;          // own 128 rows of one 64-wide k-block
   constexpr int BH_BOX = (BN / 2) * BK * 2;   // own half of the B tile, one k-block
@@ -1162,14 +1165,14 @@ __global__ void __launch_bounds__(192, 1)
       auto stage_and_store = [&](auto&& chunk_values) {
         uint8_t* stg = smem;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < NCH; ++c) {
           float v[32];
           chunk_values(c, v);
           epilogue_math<EPI>(p, col_base + c * 32, v);
           uint4* dst = reinterpret_cast<uint4*>(stg + row_in_tile * ROWB + c * 64);
 #pragma unroll
           for (int g = 0; g < 4; ++g)
-            dst[g] = make_uint4(pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]), pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]),
+            if (c * 32 + g * 8 < BN) dst[g] = make_uint4(pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]), pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]),
                                 pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]), pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]));
         }
         release_tmem();
@@ -1186,6 +1189,9 @@ __global__ void __launch_bounds__(192, 1)
         }
       };
       const bool staged = kStageable && p.stage_epi && seg_end == it_end;
+      if constexpr (BN % 32 != 0) {
+        if (!staged || contrib != 1) __trap();  // host picks such tiles only when staged
+      }
       if (contrib == 1 && staged) {
         stage_and_store([&](int c, float (&v)[32]) {
           uint32_t r[32];
@@ -1353,6 +1359,7 @@ struct GemmEnv {
   int fix_depth = -1;               // TK_GEMM_FIXDEPTH
   int stage_epi = -1;               // TK_GEMM_STAGE_EPI
   int ks = -1;                      // TK_GEMM_KS: k-blocks per ring stage of 160-wide tiles
+  bool no144 = false;               // TK_NO_144: keep 160-wide 4-CTA clusters
   int pf_partials = -1;             // TK_GEMM_PFPART
   GemmEnv() {
     no_skinny = getenv("TK_NO_SKINNY") != nullptr;
@@ -1367,6 +1374,7 @@ struct GemmEnv {
     if (const char* f = getenv("TK_GEMM_FIXDEPTH")) fix_depth = atoi(f);
     if (const char* f = getenv("TK_GEMM_STAGE_EPI")) stage_epi = atoi(f);
     if (const char* f = getenv("TK_GEMM_KS")) ks = atoi(f);
+    no144 = getenv("TK_NO_144") != nullptr;
     if (const char* f = getenv("TK_GEMM_PFPART")) pf_partials = atoi(f);
     if (const char* c = getenv("TK_GEMM_MAX_CTAS")) max_ctas = atoi(c);
   }
@@ -1868,6 +1876,23 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
             pl.skinny ? "skinny" : pl.pair ? "pair" : "tn", pl.bn, pl.cs, pl.clusters, pl.slots);
   TK_CHECK(ws_bytes >= pl.ws_bytes, TK_EINVAL, "gemm: workspace too small");
   TK_CHECK(pl.counters_fit, TK_EINVAL, "gemm: too many tiles for the counter region");
+  GemmPlan pl144 = pl;
+  if (pl.pair && pl.bn == 160 && pl.total_iters == static_cast<long long>(pl.clusters) * pl.kbs &&
+      (epi == EPI_BF16 || epi == EPI_BF16_BIAS || epi == EPI_BF16_BIAS_RELU) &&
+      genv().stage_epi != 0 && !genv().no144 && max_ctas <= 0) {
+    // A one-wave data-parallel 160-wide schedule on 4-CTA clusters leaves 20 SMs idle
+    // (<= 33 clusters fit): 144-wide tiles on 2-CTA clusters cover the same GEMM with
+    // up to 74 pairs (O-proj at M=512: 72 pairs, 144 SMs).
+    const int tn = (N + 143) / 144, groups = pl.tiles_m / 2;
+    const int cmax = max_pair_clusters(2);
+    if (tn * groups <= cmax && 10 * tn * groups >= 9 * cmax) {
+      pl144.bn = 144;
+      pl144.cs = 2;
+      pl144.tiles_n = tn;
+      pl144.clusters = tn * groups;
+      pl144.total_iters = static_cast<long long>(groups) * tn * pl.kbs;
+    }
+  }
   if (pl.skinny) {
     CUtensorMap tw, tx;
     int rc = make_tmap_kmajor(&tw, B, N, K, 128);
@@ -1930,6 +1955,14 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   if (pl.pair) {
     // each CTA loads 64-row (CS=4) or 128-row (CS=2) slices of its B half
     CUtensorMap tb;
+    if (pl144.bn == 144) {
+      a.tiles_n = pl144.tiles_n;
+      a.cs = 2;
+      a.total_iters = pl144.total_iters;
+      rc = make_tmap_kmajor(&tb, B, N, K, 72);
+      if (rc) return rc;
+      return pair_epi<2, 144>(ta, tb, a, pl144.clusters, stream, pl.ks);
+    }
     rc = make_tmap_kmajor(&tb, B, N, K, pl.bn / 2 / (pl.cs / 2));
     if (rc) return rc;
     if (pl.bn == 160) {
