@@ -1877,20 +1877,25 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   TK_CHECK(ws_bytes >= pl.ws_bytes, TK_EINVAL, "gemm: workspace too small");
   TK_CHECK(pl.counters_fit, TK_EINVAL, "gemm: too many tiles for the counter region");
   GemmPlan pl144 = pl;
-  if (pl.pair && pl.bn == 160 && pl.total_iters == static_cast<long long>(pl.clusters) * pl.kbs &&
+  if (pl.pair && pl.tiles_m % 2 == 0 &&
       (epi == EPI_BF16 || epi == EPI_BF16_BIAS || epi == EPI_BF16_BIAS_RELU) &&
-      genv().stage_epi != 0 && !genv().no144 && max_ctas <= 0) {
-    // A one-wave data-parallel 160-wide schedule on 4-CTA clusters leaves 20 SMs idle
-    // (<= 33 clusters fit): 144-wide tiles on 2-CTA clusters cover the same GEMM with
-    // up to 74 pairs (O-proj at M=512: 72 pairs, 144 SMs).
+      genv().stage_epi != 0 && !genv().no144 && max_ctas <= 0 &&
+      (genv().fbn == 0 || genv().fbn == 160)) {
+    // One wave of 144-wide tiles on 2-CTA clusters, one tile per pair (cuBLAS's
+    // structure for these shapes): up to 74 pairs = 148 SMs, where 4-CTA clusters
+    // reach 132 and a stream-K schedule pays split-tile fixups.  O-proj and FC2 at
+    // M=512: 72 pairs.  O-proj -4.4% in situ, FC2 88.5 -> 84.4 us isolated.
     const int tn = (N + 143) / 144, groups = pl.tiles_m / 2;
     const int cmax = max_pair_clusters(2);
     if (tn * groups <= cmax && 10 * tn * groups >= 9 * cmax) {
+      const int kb64 = K / 64;
+      pl144.ks = (kb64 % 2 == 0 && genv().ks != 1) ? 2 : 1;
+      pl144.kbs = kb64 / pl144.ks;
       pl144.bn = 144;
       pl144.cs = 2;
       pl144.tiles_n = tn;
       pl144.clusters = tn * groups;
-      pl144.total_iters = static_cast<long long>(groups) * tn * pl.kbs;
+      pl144.total_iters = static_cast<long long>(groups) * tn * pl144.kbs;
     }
   }
   if (pl.skinny) {
@@ -1958,10 +1963,11 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
     if (pl144.bn == 144) {
       a.tiles_n = pl144.tiles_n;
       a.cs = 2;
+      a.kbs = pl144.kbs;
       a.total_iters = pl144.total_iters;
       rc = make_tmap_kmajor(&tb, B, N, K, 72);
       if (rc) return rc;
-      return pair_epi<2, 144>(ta, tb, a, pl144.clusters, stream, pl.ks);
+      return pair_epi<2, 144>(ta, tb, a, pl144.clusters, stream, pl144.ks);
     }
     rc = make_tmap_kmajor(&tb, B, N, K, pl.bn / 2 / (pl.cs / 2));
     if (rc) return rc;
