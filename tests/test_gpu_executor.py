@@ -141,3 +141,21 @@ def test_cuda_executor_flip_keeps_device_state(tmp_path):
         assert 5_000 <= rec.latency_us <= 7_000
     for iid, pool in ex.pools.items():
         assert len(pool.free) == pool.n_pages, iid
+
+
+def test_cuda_executor_streaming_two_by_two_colocated():
+    """kv_streaming=chunk with 2 prefill + 2 decode instances sharing one device:
+    every request completes and every physical page returns to its pool."""
+    cfg = tk.config_from_dict({
+        "executor": "cuda", "kv_streaming": "chunk", "cluster": {"prefill": 2, "decode": 2},
+        "workload": {"n_requests": 24, "mixture": {"HPLD": 0.5, "LPLD": 0.5},
+                     "lengths": {"heavy_prompt": {"hi": 800}}},
+        "cost_model": {"preset": "nvlink300", "mem_capacity_tokens": 16000},
+        "model": {"name": "tiny", "prefill_pages": 512, "staging_pages": 256,
+                  "max_decode_batch": 32}})
+    ex = make_executor(cfg)
+    res = run_experiment(cfg, seed=3, executor=ex)
+    assert res.summary["completed"] == 24
+    assert not ex._streams
+    for iid, pool in ex.pools.items():
+        assert len(pool.free) == pool.n_pages, iid

@@ -79,3 +79,30 @@ def test_mixed_workload_completes_and_is_deterministic(n_prefill, n_decode):
                                                  "workload": {"n_requests": 64}}), seed=4)
     # the handoff tail shrinks; prefill-side timing is the same work
     assert a.summary["jct"]["avg_us"] <= off.summary["jct"]["avg_us"] * 1.02
+
+
+def _two_waves(tmp_path, prompt=1500):
+    lines = ["arrival_us,prompt_len,decode_len"]
+    for wave in (0, 1_500_000):
+        lines += [f"{wave},{prompt + 37 * i},{10 + i}" for i in range(8)]
+    path = tmp_path / "waves.csv"
+    path.write_text("\n".join(lines) + "\n")
+    return path
+
+
+def test_streaming_with_flips_completes(tmp_path):
+    """Flips (pdsim/control.py:408-482) with streamed handoffs in flight: a decode
+    instance being drained is excluded from dispatch, so streams only target live
+    decode instances; every request completes."""
+    cfg = tk.config_from_dict({
+        "cluster": {"prefill": 2, "decode": 2},
+        "workload": {"class": "Trace", "trace_path": str(_two_waves(tmp_path))},
+        "flip": {"enabled": True, "threshold": 0.5, "window_us": 400_000},
+        "cost_model": {"t_chunk_us": 2_000, "t_prefill_overhead_us": 50, "decode_a_us": 200,
+                       "decode_b_us": 5, "decode_c_us_per_token": 0.001},
+        "kv_streaming": "chunk", "max_events": 2_000_000})
+    res = tk.run_experiment(cfg, seed=4)
+    assert res.summary["completed"] == 16
+    assert res.summary["flips_completed"] >= 1
+    for row in res.rows:
+        assert row["ttft_us"] <= row["jct_us"]
