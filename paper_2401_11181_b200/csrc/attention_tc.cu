@@ -574,30 +574,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
-// Merge the pieces of every split (pair, head): one warp per query row, each
-// lane 4 of the 128 dims; up to 4 pieces are loaded at once (one round trip
-// for the usual 2-3), partial rows read coalesced (512 B per piece-row).
+// Merge the pieces of every split (pair, head): half a warp per query row, each
+// lane 8 of the 128 dims (16-byte bf16 loads); up to 4 pieces are loaded at once (one
+// round trip for the usual 2-3), partial rows read coalesced (256 B per piece-row).
 __global__ void __launch_bounds__(256)
     fa_combine_kernel(__nv_bfloat16* __restrict__ o, const FaPair* __restrict__ pairs,
                       const FaGroup* __restrict__ groups, int n_heads,
                       const float* __restrict__ partial) {
   griddep_launch();
   griddep_wait();  // partials of the attention kernel
-  const FaGroup g = groups[blockIdx.x >> 5];
-  const int t = (blockIdx.x >> 4) & 1, rg = blockIdx.x & 15;
+  const FaGroup g = groups[blockIdx.x >> 4];
+  const int t = (blockIdx.x >> 3) & 1, rg = blockIdx.x & 7;
   const FaPair pr = pairs[g.pair];
   const int nrows = t ? pr.nrows1 : pr.nrows0;
-  const int r = rg * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int r = rg * 16 + static_cast<int>(threadIdx.x >> 4), lane = threadIdx.x & 15;
   if (r >= nrows) return;
   auto row_of = [&](int x) {
     return reinterpret_cast<const uint8_t*>(partial) +
            ((static_cast<size_t>(g.first_piece + x) * 2 + t) * kRows + r) * kPartRowBytes;
   };
   float M = -INFINITY, L = 0.f;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
   for (int base = 0; base < g.n_pieces; base += 4) {
     float m[4], l[4];
-    float4 v[4];
+    uint4 raw[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (base + k < g.n_pieces) {
@@ -605,35 +607,41 @@ __global__ void __launch_bounds__(256)
         const float2 ml = __ldcg(reinterpret_cast<const float2*>(src + kD * 2));
         m[k] = ml.x;
         l[k] = ml.y;
-        const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(src) + lane);
-        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-        v[k] = make_float4(lo.x, lo.y, hi.x, hi.y);
+        raw[k] = __ldcg(reinterpret_cast<const uint4*>(src) + lane);
       } else {
         m[k] = -INFINITY;
         l[k] = 0.f;
-        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        raw[k] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
     const float Mn = fmaxf(fmaxf(M, fmaxf(m[0], m[1])), fmaxf(m[2], m[3]));
     if (Mn == -INFINITY) continue;
     const float c = (M == -INFINITY) ? 0.f : exp2f(M - Mn);
     L *= c;
-    acc.x *= c; acc.y *= c; acc.z *= c; acc.w *= c;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] *= c;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float w = (m[k] == -INFINITY) ? 0.f : exp2f(m[k] - Mn);
       L += w * l[k];
-      acc.x += w * v[k].x; acc.y += w * v[k].y; acc.z += w * v[k].z; acc.w += w * v[k].w;
+      const uint32_t wd[4] = {raw[k].x, raw[k].y, raw[k].z, raw[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wd[j]));
+        acc[2 * j] += w * f.x;
+        acc[2 * j + 1] += w * f.y;
+      }
     }
     M = Mn;
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
-  uint2 pk;
-  pk.x = pack_bf16x2(acc.x * inv, acc.y * inv);
-  pk.y = pack_bf16x2(acc.z * inv, acc.w * inv);
-  *reinterpret_cast<uint2*>(o + static_cast<size_t>(pr.row0 + t * kRows + r) * n_heads * kD +
-                            g.head * kD + lane * 4) = pk;
+  uint4 pk;
+  pk.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+  pk.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+  pk.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+  pk.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+  *reinterpret_cast<uint4*>(o + static_cast<size_t>(pr.row0 + t * kRows + r) * n_heads * kD +
+                            g.head * kD + lane * 8) = pk;
 }
 
 // ------------------------------------------------------------------ host side
@@ -771,7 +779,7 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   TK_CUDA(cudaGetLastError());
   note_launch();
   if (plan.n_groups > 0) {
-    TK_CUDA(launch_pdl(fa_combine_kernel, dim3(plan.n_groups * 32), dim3(256), 0, s, o,
+    TK_CUDA(launch_pdl(fa_combine_kernel, dim3(plan.n_groups * 16), dim3(256), 0, s, o,
                        pairs_dev, groups_dev, g.n_heads, partial));
     TK_CUDA(cudaGetLastError());
     note_launch();
