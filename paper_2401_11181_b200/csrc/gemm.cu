@@ -67,6 +67,7 @@ struct GemmArgs {
   long long total_iters;
   int b_pol;      // weights' L2 policy: 0 evict_first (read once), 1 evict_normal, 2 evict_last
   int pf_dist;    // k-blocks of weight L2 prefetch ahead of the TMA ring (0: none)
+  int entry_pf;   // L2-prefetch the first ring fill's weights at kernel entry (TK_GEMM_ENTRY_PF)
   int pf_partials;  // TK_GEMM_PFPART: L2-prefetch a final piece's partials (measured: no gain)
   int stage_epi;  // last tile's bf16 epilogue staged in shared memory (TK_GEMM_STAGE_EPI=0: off)
   int fix_depth;  // stream-K fixup: partial chunks in flight (1, or 2 = fixup_epilogue_deep)
@@ -935,6 +936,20 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
+    if (p.entry_pf) {
+      // The first ring fill's weight tiles come from DRAM: start pulling them into L2
+      // now, while the barriers, TMEM and the cluster are being set up.
+      const int cl = blockIdx.x / CS, g = gridDim.x / CS, gm = p.tiles_m / CS;
+      const long long b0 = static_cast<long long>(cl) * p.total_iters / g;
+      const long long b1 = static_cast<long long>(cl + 1) * p.total_iters / g;
+      int ct = static_cast<int>(b0 / p.kbs), kq = static_cast<int>(b0 % p.kbs);
+      for (long long i = b0; i < b1 && i < b0 + STAGES; ++i) {
+        const int row = (ct / gm) * BN + half * (BN / 2) + pair * ((BN / 2) / (CS / 2));
+#pragma unroll
+        for (int s = 0; s < KS; ++s) tma_prefetch_2d(&tmap_b, (kq * KS + s) * BK, row);
+        if (++kq == p.kbs) { kq = 0; ++ct; }
+      }
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);        // leader: its expect_tx arrive (+ all TMA bytes of the pair)
       mbar_init(&empty[s], NPAIRS);  // one MMA-commit arrive per pair reading this stage
@@ -1359,6 +1374,7 @@ struct GemmEnv {
   int fix_depth = -1;               // TK_GEMM_FIXDEPTH
   int stage_epi = -1;               // TK_GEMM_STAGE_EPI
   int ks = -1;                      // TK_GEMM_KS: k-blocks per ring stage of 160-wide tiles
+  int entry_pf = -1;                // TK_GEMM_ENTRY_PF
   bool no144 = false;               // TK_NO_144: keep 160-wide 4-CTA clusters
   int pf_partials = -1;             // TK_GEMM_PFPART
   GemmEnv() {
@@ -1374,6 +1390,7 @@ struct GemmEnv {
     if (const char* f = getenv("TK_GEMM_FIXDEPTH")) fix_depth = atoi(f);
     if (const char* f = getenv("TK_GEMM_STAGE_EPI")) stage_epi = atoi(f);
     if (const char* f = getenv("TK_GEMM_KS")) ks = atoi(f);
+    if (const char* f = getenv("TK_GEMM_ENTRY_PF")) entry_pf = atoi(f);
     no144 = getenv("TK_NO_144") != nullptr;
     if (const char* f = getenv("TK_GEMM_PFPART")) pf_partials = atoi(f);
     if (const char* c = getenv("TK_GEMM_MAX_CTAS")) max_ctas = atoi(c);
@@ -1949,6 +1966,7 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   a.wait_mode = genv().wait_mode >= 0 ? genv().wait_mode : 0;
   a.fix_depth = genv().fix_depth >= 0 ? genv().fix_depth : 1;
   a.stage_epi = genv().stage_epi >= 0 ? genv().stage_epi : 1;
+  a.entry_pf = genv().entry_pf >= 0 ? genv().entry_pf : 0;  // measured: slightly slower
   a.pf_partials = genv().pf_partials >= 0 ? genv().pf_partials : 0;
   a.slots = pl.slots;
   a.total_iters = pl.total_iters;
