@@ -1970,8 +1970,6 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
   a.pf_partials = genv().pf_partials >= 0 ? genv().pf_partials : 0;
   a.slots = pl.slots;
   a.total_iters = pl.total_iters;
-  const int64_t tiles = static_cast<int64_t>(a.tiles_m) * a.tiles_n;
-  (void)tiles;
   a.counters = static_cast<int*>(workspace);
   a.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
   a.kv = scatter ? *scatter : QkvScatter{};
