@@ -750,7 +750,10 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
     FaGroup* groups = pk.put<FaGroup>(nullptr, pcap * m.n_heads, &fa_groups_d);
     int32_t* off = pk.put<int32_t>(nullptr, kNumSMs + 1, &fa_off_d);
     TK_CHECK(pk.ok(), TK_EINVAL, "prefill: metadata exceeds staging slot");
-    TK_CHECK(build_fa_plan(slices, n_slices, m.n_heads, kNumSMs, &fa, pairs, pcap, units, ucap,
+    // attention CTAs (TK_FA_CTAS caps them, experiments)
+    static const int fa_ctas = getenv("TK_FA_CTAS") ? std::max(1, std::min(kNumSMs, atoi(getenv("TK_FA_CTAS"))))
+                                                    : kNumSMs;
+    TK_CHECK(build_fa_plan(slices, n_slices, m.n_heads, fa_ctas, &fa, pairs, pcap, units, ucap,
                            groups, pcap * m.n_heads, off, kNumSMs + 1) == 0,
              TK_EINVAL, "prefill: attention plan overflow");
   } else {
