@@ -132,6 +132,12 @@ int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
  * = argmax over the instance's n_labels classes.                             */
 int tk_predict(tk_instance* inst, const int32_t* token_ids, const int32_t* lens, int32_t n,
                int32_t max_len, int32_t* bucket_out, tk_event** ev);
+/* Same classification, also returning the fp32 class scores [n, n_labels]
+ * (row-major; the call waits for them).  Parity tests compare these with the
+ * oracle's logits instead of the argmax alone.                               */
+int tk_predict_scores(tk_instance* inst, const int32_t* token_ids, const int32_t* lens,
+                      int32_t n, int32_t max_len, int32_t* bucket_out, float* scores_out,
+                      tk_event** ev);
 /* Swap whole requests' pages to / from pinned host memory (page_bytes each). */
 int tk_swap_out(tk_instance* inst, const int32_t* pages, int32_t n, void* pinned_host,
                 tk_event** ev);

@@ -136,22 +136,26 @@ class PagedCache:
     shape: Shape
     n_pages: int
     page_tokens: int = 16
+    device: str = "cpu"
     pages: torch.Tensor = field(init=False)
 
     def __post_init__(self):
         s = self.shape
         self.pages = torch.zeros(self.n_pages, s.n_layers, 2, s.n_heads, self.page_tokens,
-                                 s.head_dim)
+                                 s.head_dim, device=self.device)
 
     def write(self, layer: int, table: list[int], positions: torch.Tensor, k: torch.Tensor,
               v: torch.Tensor) -> None:
         pt = self.page_tokens
-        for i, p in enumerate(positions.tolist()):
-            self.pages[table[p // pt], layer, 0, :, p % pt] = k[i]
-            self.pages[table[p // pt], layer, 1, :, p % pt] = v[i]
+        pos = positions.to(self.device)
+        page = torch.tensor(table, dtype=torch.long, device=self.device)[pos // pt]
+        slot = pos % pt
+        self.pages[page, layer, 0, :, slot] = k
+        self.pages[page, layer, 1, :, slot] = v
 
     def read(self, layer: int, table: list[int], n: int) -> tuple[torch.Tensor, torch.Tensor]:
-        idx = torch.tensor(table[: (n + self.page_tokens - 1) // self.page_tokens])
+        idx = torch.tensor(table[: (n + self.page_tokens - 1) // self.page_tokens],
+                           device=self.device)
         kv = self.pages[idx, layer]  # [np, 2, H, pt, D]
         k = kv[:, 0].permute(1, 0, 2, 3).reshape(self.shape.n_heads, -1, self.shape.head_dim)[:, :n]
         v = kv[:, 1].permute(1, 0, 2, 3).reshape(self.shape.n_heads, -1, self.shape.head_dim)[:, :n]
@@ -161,14 +165,22 @@ class PagedCache:
 class OracleModel:
     """fp32 forward with the device's chunked, paged execution order."""
 
-    def __init__(self, shape: Shape, weights: dict[str, torch.Tensor]):
+    def __init__(self, shape: Shape, weights: dict[str, torch.Tensor], device: str = "cpu"):
         self.s = shape
-        self.w = {k: v.float() for k, v in weights.items()}
+        self.device = device
+        self.w = {k: v.float().to(device) for k, v in weights.items()}
 
     @classmethod
-    def from_instance(cls, shape: Shape, inst) -> "OracleModel":
+    def from_instance(cls, shape: Shape, inst, device: str = "cpu") -> "OracleModel":
+        """Weights read back from a device instance.  ``device="cuda"`` runs the
+        same fp32 arithmetic on the GPU (TF32 off) so the OPT-13B-width parity
+        tests finish in seconds; it is still the checker, never the product."""
+        if device != "cpu":
+            torch.backends.cuda.matmul.allow_tf32 = False
+            torch.backends.cudnn.allow_tf32 = False
         ws = weight_shapes(shape)
-        return cls(shape, {n: bf16_bits_to_f32(inst.read_weight(n)).view(ws[n]) for n in ws})
+        return cls(shape, {n: bf16_bits_to_f32(inst.read_weight(n)).view(ws[n]) for n in ws},
+                   device)
 
     # -- pieces ----------------------------------------------------------------
     def _norm(self, x, prefix):
@@ -181,7 +193,8 @@ class OracleModel:
 
     def _rope(self, x, pos):  # x [n, H, D]
         D = self.s.head_dim
-        inv = self.s.rope_theta ** (-torch.arange(0, D, 2, dtype=torch.float32) / D)
+        inv = self.s.rope_theta ** (-torch.arange(0, D, 2, dtype=torch.float32,
+                                                  device=x.device) / D)
         ang = pos[:, None].float() * inv[None, :]
         cos, sin = torch.cat([ang.cos()] * 2, -1)[:, None], torch.cat([ang.sin()] * 2, -1)[:, None]
         x1, x2 = x[..., : D // 2], x[..., D // 2:]
@@ -212,7 +225,7 @@ class OracleModel:
             n_ctx = int(pos[-1]) + 1
             K, V = cache.read(l, table, n_ctx)
             sc = torch.einsum("qhd,hkd->hqk", qi, K) * D ** -0.5
-            mask = torch.arange(n_ctx)[None, :] > pos[:, None]
+            mask = torch.arange(n_ctx, device=x.device)[None, :] > pos[:, None]
             sc = sc.masked_fill(mask[None], float("-inf"))
             attn[sl] = torch.einsum("hqk,hkd->qhd", torch.softmax(sc, -1), V)
         o = attn.reshape(-1, h) @ w[p + ("self_attn.out_proj.weight" if opt else "self_attn.o_proj.weight")].t()
@@ -244,10 +257,11 @@ class OracleModel:
 
         Returns fp32 logits of the emitting slices' last tokens, in slice order.
         """
-        ids = torch.tensor(token_ids, dtype=torch.long)
+        dev = self.device
+        ids = torch.tensor(token_ids, dtype=torch.long, device=dev)
         pos_all, rows, row = [], [], 0
         for start, n, bto, npg, _ in slices:
-            pos = torch.arange(start, start + n)
+            pos = torch.arange(start, start + n, device=dev)
             pos_all.append(pos)
             rows.append((list(block_tables[bto:bto + npg]), pos, slice(row, row + n)))
             row += n
@@ -262,8 +276,8 @@ class OracleModel:
     @torch.no_grad()
     def decode_step(self, cache: PagedCache, last_tokens, ctx_lens, tables) -> torch.Tensor:
         """Mirror of tk_decode_step; returns fp32 logits [B, V]."""
-        ids = torch.tensor(last_tokens, dtype=torch.long)
-        pos = torch.tensor(ctx_lens, dtype=torch.long)
+        ids = torch.tensor(last_tokens, dtype=torch.long, device=self.device)
+        pos = torch.tensor(ctx_lens, dtype=torch.long, device=self.device)
         rows = [(tables[b], pos[b:b + 1], slice(b, b + 1)) for b in range(len(last_tokens))]
         x = self.embed(ids, pos)
         for l in range(self.s.n_layers):
@@ -275,10 +289,10 @@ class OracleModel:
         """Whole-prompt logits [n, V] without paging (for the transformers pin)."""
         n = len(token_ids)
         pt = 16
-        cache = PagedCache(self.s, (n + pt - 1) // pt, pt)
+        cache = PagedCache(self.s, (n + pt - 1) // pt, pt, device=self.device)
         table = list(range(cache.n_pages))
-        ids = torch.tensor(token_ids, dtype=torch.long)
-        pos = torch.arange(n)
+        ids = torch.tensor(token_ids, dtype=torch.long, device=self.device)
+        pos = torch.arange(n, device=self.device)
         x = self.embed(ids, pos)
         for l in range(self.s.n_layers):
             x = self.layer(l, x, [(table, pos, slice(0, n))], cache)

@@ -758,11 +758,7 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
               : variant == 10 ? (KernFn)chunk_attn_fa_kernel<3, false, 0, 3>
               : variant == 11 ? (KernFn)chunk_attn_fa_kernel<2, false, 0, 3>
                              : (KernFn)chunk_attn_fa_kernel<4, false, 0, 3>;
-  static bool cfg = false;
-  if (!cfg) {
-    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    cfg = true;
-  }
+  TK_SMEM_OPT_IN(kern, kSmem);
   FaParams prm;
   prm.pairs = pairs_dev;
   prm.units = units_dev;

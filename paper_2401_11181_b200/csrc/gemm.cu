@@ -15,10 +15,16 @@
 //
 // Work split: the (tile, k-block) iteration space is divided evenly over the
 // persistent CTAs (stream-K).  A tile owned by one CTA is written directly;
-// a tile shared by several CTAs is reduced through an fp32 workspace with
-// float4 atomics, and the last contributor to arrive (per-tile counter)
-// applies the epilogue and re-zeroes the workspace.  Nobody ever waits on a
-// peer CTA, so the scheme is deadlock-free at any occupancy.  This fixes the
+// a tile shared by several CTAs is reduced without atomics on the data: each
+// contributor takes an arrival number from a per-tile counter; every arrival
+// but the last stores its fp32 partial into its own slot of the workspace
+// (thread-major, 512 contiguous bytes per warp access) and raises its
+// ready flag with a release store; the last arrival acquires the earlier
+// flags, adds their partials to its TMEM accumulator, runs the epilogue and
+// re-zeroes the counter and flags.  The last arrival only ever waits on CTAs
+// that already hold an arrival number (i.e. are running and past their MMAs),
+// so the scheme is deadlock-free at any occupancy, including when another
+// instance's kernels share the GPU.  This fixes the
 // wave quantisation of M=512 chunk GEMMs (e.g. 80 tiles of 128x256 at
 // N=5120 on 148 SMs) and of skinny decode GEMMs alike.
 //
@@ -1648,12 +1654,7 @@ static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const Gem
                          int ctas, cudaStream_t stream) {
   using Cfg = SkinnyCfg<NB>;
   auto kern = gemm_skinny_kernel<NB, EPI>;
-  static bool configured = false;
-  if (!configured) {
-    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM_BYTES));
-    configured = true;
-  }
+  TK_SMEM_OPT_IN(kern, Cfg::SMEM_BYTES);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(Cfg::THREADS);
@@ -1686,12 +1687,7 @@ template <int EPI, int CS, int BN, int KS>
 static int launch_pair_ks(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                           int clusters, cudaStream_t stream) {
   auto kern = gemm_pair_kernel<EPI, CS, BN, KS>;
-  static bool configured = false;
-  if (!configured) {
-    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 PairCfg<BN, KS>::SMEM));
-    configured = true;
-  }
+  TK_SMEM_OPT_IN(kern, PairCfg<BN, KS>::SMEM);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * CS);
   cfg.blockDim = dim3(192);
@@ -1779,12 +1775,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
                        int clusters, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_tn_kernel<BN, EPI, CS>;
-  static bool configured = false;
-  if (!configured) {
-    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM_BYTES));
-    configured = true;
-  }
+  TK_SMEM_OPT_IN(kern, Cfg::SMEM_BYTES);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * CS);
   cfg.blockDim = dim3(Cfg::THREADS);

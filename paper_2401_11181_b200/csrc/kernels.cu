@@ -666,12 +666,7 @@ int launch_chunk_attention_work(const __nv_bfloat16* q, int q_stride, __nv_bfloa
   dim3 grid(n_work, g.n_heads);
   if (g.head_dim == 128) {
     const int smem = 4 * kAttnBlock * 128 * 2;
-    static bool cfg = false;
-    if (!cfg) {
-      TK_CUDA(cudaFuncSetAttribute(chunk_attn_kernel<128>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cfg = true;
-    }
+    TK_SMEM_OPT_IN(chunk_attn_kernel<128>, smem);
     chunk_attn_kernel<128><<<grid, kAttnThreads, smem, s>>>(q, q_stride, o, pool, g, layer, work,
                                                             qblocks, slices_dev, bt_dev,
                                                             scale_log2, partial);

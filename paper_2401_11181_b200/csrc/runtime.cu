@@ -345,7 +345,30 @@ static int take_slot(tk_instance* inst, Slot** out) {
   return TK_OK;
 }
 
+// Released events whose device work had not finished yet (handoff / swap
+// events own no staging slot).  Releasing must not block the host -- a
+// streamed handoff drops each part's handle while the copy still runs behind
+// the next chunk -- so they are parked here and freed once complete.
+static std::mutex g_zombie_mu;
+static std::vector<tk_event*> g_zombies;
+
+static void sweep_zombies() {
+  std::lock_guard<std::mutex> lock(g_zombie_mu);
+  size_t keep = 0;
+  for (tk_event* ev : g_zombies) {
+    if (cudaEventQuery(ev->end) == cudaSuccess) {
+      ev->finished = true;
+      maybe_free_event(ev);
+    } else {
+      g_zombies[keep++] = ev;
+    }
+  }
+  cudaGetLastError();  // a not-ready query is not an error
+  g_zombies.resize(keep);
+}
+
 static int new_event(tk_instance* inst, cudaStream_t s, tk_event** out) {
+  if (!g_zombies.empty()) sweep_zombies();
   tk_event* ev = new tk_event();
   ev->device = inst->device;
   TK_CUDA(cudaEventCreate(&ev->start));
@@ -984,8 +1007,9 @@ int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
 }
 
 // ------------------------------------------------------------------ predictor
-int tk_predict(tk_instance* inst, const int32_t* token_ids, const int32_t* lens, int32_t n,
-               int32_t max_len, int32_t* bucket_out, tk_event** ev) {
+static int predict_impl(tk_instance* inst, const int32_t* token_ids, const int32_t* lens,
+                        int32_t n, int32_t max_len, int32_t* bucket_out, float* scores_out,
+                        tk_event** ev) {
   TK_CHECK(inst && ev && token_ids && lens && n > 0, TK_EINVAL, "tk_predict: null argument");
   TK_CHECK(inst->w->md.n_labels > 0, TK_EINVAL, "tk_predict: instance has no classifier head");
   const int pt = inst->geom.page_tokens;
@@ -1005,7 +1029,20 @@ int tk_predict(tk_instance* inst, const int32_t* token_ids, const int32_t* lens,
   TK_CHECK(static_cast<int>(bt.size()) <= inst->kv_pages, TK_ECAPACITY,
            "tk_predict: prompts exceed the predictor's page pool");
   return prefill_impl(inst, inst->s_pred, static_cast<int32_t>(ids.size()), ids.data(), sl.data(),
-                      n, bt.data(), static_cast<int32_t>(bt.size()), bucket_out, nullptr, ev, true);
+                      n, bt.data(), static_cast<int32_t>(bt.size()), bucket_out, scores_out, ev,
+                      true);
+}
+
+int tk_predict(tk_instance* inst, const int32_t* token_ids, const int32_t* lens, int32_t n,
+               int32_t max_len, int32_t* bucket_out, tk_event** ev) {
+  return predict_impl(inst, token_ids, lens, n, max_len, bucket_out, nullptr, ev);
+}
+
+int tk_predict_scores(tk_instance* inst, const int32_t* token_ids, const int32_t* lens,
+                      int32_t n, int32_t max_len, int32_t* bucket_out, float* scores_out,
+                      tk_event** ev) {
+  TK_CHECK(scores_out, TK_EINVAL, "tk_predict_scores: null scores_out");
+  return predict_impl(inst, token_ids, lens, n, max_len, bucket_out, scores_out, ev);
 }
 
 // ------------------------------------------------------------------ swap
@@ -1097,13 +1134,19 @@ int tk_event_wait(tk_event* ev, int64_t* elapsed_ns) {
 
 int tk_event_release(tk_event* ev) {
   if (!ev) return TK_OK;
-  ev->released = true;
-  if (ev->slot == nullptr || ev->finished) {
-    if (!ev->finished) {
-      int rc = finalize_event(ev);
-      if (rc) return rc;
-    }
+  ev->released = true;  // host outputs are abandoned from here on
+  if (ev->finished) {
     maybe_free_event(ev);
+  } else if (ev->slot == nullptr) {
+    // no slot to free it later: never block here, park it until it completes
+    if (cudaEventQuery(ev->end) == cudaSuccess) {
+      ev->finished = true;
+      maybe_free_event(ev);
+    } else {
+      cudaGetLastError();
+      std::lock_guard<std::mutex> lock(g_zombie_mu);
+      g_zombies.push_back(ev);
+    }
   }
   // otherwise the owning slot frees it when it is finalized on reuse
   return TK_OK;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 #include <string>
 
@@ -33,6 +34,23 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
   } while (0)
 
 constexpr int kNumSMs = 148;
+
+// Dynamic shared memory above 48 KB is an opt-in per kernel *per device
+// context*: one process drives every GPU of the box (a 2:6 prefill:decode
+// split, NVLink handoff), so each call site remembers which devices it has
+// configured in a bitmask instead of a process-wide flag.
+#define TK_SMEM_OPT_IN(kern, ...)                                                    \
+  do {                                                                               \
+    static std::atomic<uint64_t> _tk_cfg_mask{0};                                    \
+    int _tk_dev = 0;                                                                 \
+    TK_CUDA(cudaGetDevice(&_tk_dev));                                                \
+    const uint64_t _tk_bit = 1ull << (_tk_dev & 63);                                 \
+    if (!(_tk_cfg_mask.load(std::memory_order_acquire) & _tk_bit)) {                 \
+      TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   (__VA_ARGS__)));                                  \
+      _tk_cfg_mask.fetch_or(_tk_bit, std::memory_order_release);                     \
+    }                                                                                \
+  } while (0)
 
 // ---------------------------------------------------------------- smem / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

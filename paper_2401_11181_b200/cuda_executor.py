@@ -128,6 +128,11 @@ class CudaExecutor:
         self.first_token: dict[int, int] = {}
         self.last_token: dict[int, int] = {}
         self.swap_host: dict[int, tuple[int, int]] = {}       # req -> (pinned ptr, pages)
+        # receive staging (arrived, not yet admitted): pages held per decode instance,
+        # bounded by staging_pages; beyond it the KV waits in pinned host memory
+        self.staged: dict[str, int] = {}                      # inst -> staged pages
+        self.staged_of: dict[int, int] = {}                   # req -> its staged pages
+        self.host_staged: set[int] = set()                    # reqs staged in host memory
         self._streams: dict[int, dict] = {}                   # req -> streamed handoff state
         self.predictors: dict[int, native.Instance] = {}
         self.prompts: dict[int, list[int]] = {}
@@ -248,11 +253,24 @@ class CudaExecutor:
         if src_id is None or req.id not in self.tables.get(src_id, {}):
             raise SimulationError(f"request {req.id}: no KV to transfer")
         src_pages = self.tables[src_id].pop(req.id)
+        self.kv_home[req.id] = dst
+        nbytes = len(src_pages) * self.insts[src_id].page_bytes
+        if not self._stage_on_device(dst, req.id, len(src_pages)):
+            # receive staging full (arrivals queue without bound in pdsim's decode
+            # instance): park the KV in pinned host memory; admission restores it
+            ptr = native.host_alloc(nbytes)
+            ev = self.insts[src_id].swap_out(src_pages, ptr)
+            self.swap_host[req.id] = (ptr, len(src_pages))
+            self.host_staged.add(req.id)
+            self.stats["kv_host_staged"] = self.stats.get("kv_host_staged", 0) + 1
+
+            def release_src_host():
+                self.pools[src_id].give(src_pages)
+
+            return _Then(ev, release_src_host)
         dst_pages = self.pools[dst].take(len(src_pages), dst)  # receive staging
         self.tables[dst][req.id] = dst_pages
-        self.kv_home[req.id] = dst
         ev = self.insts[src_id].kv_send(src_pages, self.insts[dst], dst_pages)
-        nbytes = len(src_pages) * self.insts[src_id].page_bytes
         self.stats["kv_bytes_sent"] += nbytes
 
         def release_src():
@@ -269,22 +287,35 @@ class CudaExecutor:
         in order on the source's copy stream, each after the chunk that wrote it."""
         src_id = src_inst.id
         src_pages = self.tables[src_id][req.id]
+        pb = self.insts[src_id].page_bytes
         st = self._streams.get(req.id)
         if st is None:
-            st = self._streams[req.id] = {"sent": 0,
-                                          "dst": self.pools[dst].take(len(src_pages), dst)}
-            self.tables[dst][req.id] = st["dst"]
+            st = self._streams[req.id] = {"sent": 0, "parts": []}
+            if self._stage_on_device(dst, req.id, len(src_pages)):
+                st["dst"] = self.pools[dst].take(len(src_pages), dst)
+                self.tables[dst][req.id] = st["dst"]
+            else:  # staging full: the parts collect in one pinned host buffer
+                st["host"] = native.host_alloc(len(src_pages) * pb)
         hi = len(src_pages) if final else end // self.page_tokens
         lo = st["sent"]
-        ev = self.insts[src_id].kv_send(src_pages[lo:hi], self.insts[dst], st["dst"][lo:hi])
+        if "host" in st:
+            ev = self.insts[src_id].swap_out(src_pages[lo:hi], st["host"] + lo * pb)
+        else:
+            ev = self.insts[src_id].kv_send(src_pages[lo:hi], self.insts[dst], st["dst"][lo:hi])
         st["sent"] = max(lo, hi)
-        nbytes = max(0, hi - lo) * self.insts[src_id].page_bytes
+        nbytes = max(0, hi - lo) * pb
         self.stats["kv_bytes_sent"] += nbytes
         if not final:
+            # keep the part's handle: the copy runs behind the next chunks
+            st["parts"].append(ev)
             return ev
         del self._streams[req.id]
         self.tables[src_id].pop(req.id)
         self.kv_home[req.id] = dst
+        if "host" in st:
+            self.swap_host[req.id] = (st["host"], len(src_pages))
+            self.host_staged.add(req.id)
+            self.stats["kv_host_staged"] = self.stats.get("kv_host_staged", 0) + 1
 
         def release_src():
             self.pools[src_id].give(src_pages)
@@ -293,8 +324,22 @@ class CudaExecutor:
         return _Then(ev, release_src)
 
     # -- decode side ----------------------------------------------------------------------------
+    def _stage_on_device(self, dst: str, rid: int, n: int) -> bool:
+        """Reserve ``n`` receive-staging pages of ``dst`` for request ``rid``."""
+        if self.staged.get(dst, 0) + n > self.staging_pages:
+            return False
+        self.staged[dst] = self.staged.get(dst, 0) + n
+        self.staged_of[rid] = n
+        return True
+
     def admit(self, inst, dreq) -> None:
         # staged pages become resident pages: the counts check happened in the store
+        rid = dreq.req.id
+        if rid in self.staged_of:
+            self.staged[inst.id] -= self.staged_of.pop(rid)
+        if rid in self.host_staged:  # KV parked in pinned host memory on arrival
+            self.host_staged.discard(rid)
+            self.swap_in(inst, dreq)
         have = self.tables[inst.id].get(dreq.req.id)
         need = costs.pages_needed(self.params, dreq.kv_tokens)
         if have is None:

@@ -61,6 +61,8 @@ _SIGNATURES = {
                         C.POINTER(C.c_float), C.POINTER(_P)], C.c_int),
     "tk_kv_send": ([_P, _I32P, _P, _I32P, C.c_int32, C.POINTER(_P)], C.c_int),
     "tk_predict": ([_P, _I32P, _I32P, C.c_int32, C.c_int32, _I32P, C.POINTER(_P)], C.c_int),
+    "tk_predict_scores": ([_P, _I32P, _I32P, C.c_int32, C.c_int32, _I32P, C.POINTER(C.c_float),
+                           C.POINTER(_P)], C.c_int),
     "tk_swap_out": ([_P, _I32P, C.c_int32, _P, C.POINTER(_P)], C.c_int),
     "tk_swap_in": ([_P, _I32P, C.c_int32, _P, C.POINTER(_P)], C.c_int),
     "tk_host_alloc": ([C.c_int64, C.POINTER(_P)], C.c_int),
@@ -342,6 +344,20 @@ class Instance:
         check(load().tk_predict(self._h, ids, ls, len(lens), max_len, out, C.byref(ev)),
               "tk_predict")
         return Event(ev, keep=(ids, ls, out)), out
+
+    def predict_scores(self, token_ids, lens, max_len: int = 512):
+        """(buckets, fp32 scores [n, n_labels]) -- waits for the device."""
+        import numpy as np
+        out = (C.c_int32 * len(lens))()
+        scores = np.empty((len(lens), self.shape.n_labels), dtype=np.float32)
+        ids, ls = i32(token_ids), i32(lens)
+        ev = C.c_void_p()
+        check(load().tk_predict_scores(self._h, ids, ls, len(lens), max_len, out,
+                                       scores.ctypes.data_as(C.POINTER(C.c_float)), C.byref(ev)),
+              "tk_predict_scores")
+        e = Event(ev, keep=(ids, ls, out))
+        e.wait()
+        return list(out), scores
 
     def swap_out(self, pages, host_ptr) -> Event:
         p = i32(pages)

@@ -113,93 +113,172 @@ def _gather_kv(pool, layer, pages, n_tok, pt):
     return K, V
 
 
-@pytest.mark.parametrize("ctxs", [[1], [16, 17, 300], [1000, 4097, 40, 2048, 9000]])
-def test_paged_decode_attention(ctxs):
-    g = torch.Generator(device="cuda").manual_seed(len(ctxs))
-    L, H, D, pt = 3, 8, 128, 16
+# Attention parity metric.  Per (query row, head): normwise relative error
+# ||o - ref|| / ||ref|| and cosine similarity.  Long contexts make the outputs
+# themselves small (a near-uniform softmax averages thousands of V rows), so
+# an absolute tolerance cannot see a dropped page; a normwise relative one
+# can.  bf16 output rounding alone gives ~3e-3; a dropped 16-key page, a
+# dropped 128-key block or a causal mask shifted by one give >= 4e-2 at the
+# sizes below (measured on the reference itself, and asserted as negative
+# controls in every test).  Scores are sharpened (q x4, score std ~2) so that
+# individual keys matter.
+ATTN_REL = 1e-2
+ATTN_COS = 0.9999
+Q_SHARPEN = 4.0
+
+
+def _attn_metric(got, ref):
+    """got/ref [..., D] -> (max normwise relative error, min cosine)."""
+    got, ref = got.float(), ref.float()
+    rel = (got - ref).norm(dim=-1) / ref.norm(dim=-1).clamp_min(1e-12)
+    cos = torch.nn.functional.cosine_similarity(got, ref, dim=-1)
+    return rel.max().item(), cos.min().item()
+
+
+def _attn_ok(m) -> bool:
+    return m[0] <= ATTN_REL and m[1] >= ATTN_COS
+
+
+def _ref_attention(q, K, V, qpos, scale, mask_shift=0):
+    """q [H, n, D], K/V [H, ctx, D] fp32, causal by absolute position (+ shift)."""
+    sc = torch.einsum("hqd,hkd->hqk", q, K) * scale
+    kpos = torch.arange(K.shape[1], device=q.device)[None, :]
+    sc = sc.masked_fill(kpos > qpos[:, None] + mask_shift, float("-inf"))
+    p = torch.nan_to_num(torch.softmax(sc, -1))
+    return torch.einsum("hqk,hkd->hqd", p, V)
+
+
+def _decode_case(ctxs, seed, H=8, L=3, D=128, pt=16):
+    g = torch.Generator(device="cuda").manual_seed(seed)
     n_pages = sum((c + pt - 1) // pt for c in ctxs) + 4
     pool = _pool(n_pages, L, H, D, pt, g)
     perm = torch.randperm(n_pages, generator=torch.Generator().manual_seed(0)).tolist()
     stride = max((c + pt - 1) // pt for c in ctxs)
     bt = torch.zeros(len(ctxs), stride, dtype=torch.int32)
-    cur = 0
-    tables = []
+    cur, tables = 0, []
     for b, c in enumerate(ctxs):
         np_ = (c + pt - 1) // pt
         pages = perm[cur:cur + np_]
         cur += np_
         bt[b, :np_] = torch.tensor(pages, dtype=torch.int32)
         tables.append(pages)
-    q = torch.randn(len(ctxs), H, D, device="cuda", generator=g).bfloat16()
+    q = (torch.randn(len(ctxs), H, D, device="cuda", generator=g) * Q_SHARPEN).bfloat16()
+    return pool, bt, tables, q, perm[cur:]
+
+
+@pytest.mark.parametrize("ctxs", [[1], [16, 17, 300], [1000, 4097, 40, 2048, 9000],
+                                  [8192, 3000, 10240, 511]])
+def test_paged_decode_attention(ctxs):
+    L, H, D, pt, layer = 3, 8, 128, 16, 1
+    pool, bt, tables, q, spare = _decode_case(ctxs, len(ctxs) * 7 + ctxs[0], H, L, D, pt)
     lens = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
-    layer = 1
     o = native.paged_decode_attention(q, pool, layer, L, bt.cuda(), lens, pt)
     torch.cuda.synchronize()
+    worst = (0.0, 1.0)
     for b, c in enumerate(ctxs):
         K, V = _gather_kv(pool, layer, tables[b], c, pt)
-        s = torch.einsum("hd,htd->ht", q[b].float(), K) * D ** -0.5
-        ref = torch.einsum("ht,htd->hd", torch.softmax(s, dim=-1), V)
-        assert (o[b].float() - ref).abs().max().item() < 2e-2
+        qpos = torch.tensor([c - 1], device="cuda")
+        ref = _ref_attention(q[b].float()[:, None], K, V, qpos, D ** -0.5)[:, 0]
+        m = _attn_metric(o[b], ref)
+        worst = (max(worst[0], m[0]), min(worst[1], m[1]))
+        assert _attn_ok(m), (c, m)
+        if c >= 2:  # negative control: missing the newest key must be detected
+            if c <= 64:
+                short = _ref_attention(q[b].float()[:, None], K, V, qpos, D ** -0.5, -1)[:, 0]
+                assert not _attn_ok(_attn_metric(o[b], short)), c
+    # negative control on the device: one page of the longest context replaced
+    b = max(range(len(ctxs)), key=lambda i: ctxs[i])
+    if ctxs[b] >= 64:
+        bad = bt.clone()
+        bad[b, len(tables[b]) // 2] = spare[0] if spare else tables[b][0]
+        o_bad = native.paged_decode_attention(q, pool, layer, L, bad.cuda(), lens, pt)
+        K, V = _gather_kv(pool, layer, tables[b], ctxs[b], pt)
+        ref = _ref_attention(q[b].float()[:, None], K, V, torch.tensor([ctxs[b] - 1],
+                                                                       device="cuda"),
+                             D ** -0.5)[:, 0]
+        assert not _attn_ok(_attn_metric(o_bad[b], ref)), "dropped page not detected"
+    print(f"decode attention {ctxs}: max rel {worst[0]:.2e}, min cos {worst[1]:.6f}")
 
 
-def test_chunk_attention_mixed_slices():
-    """A chunk holding a prompt tail with a long prefix, two whole prompts and a head."""
-    g = torch.Generator(device="cuda").manual_seed(5)
-    L, H, D, pt = 2, 4, 128, 16
-    # (prefix already in pages, tokens in this chunk)
-    reqs = [(394, 118), (0, 18), (0, 100), (0, 276)]
+def _chunk_case(reqs, H, seed, L=2, D=128, pt=16, scatter=True):
+    g = torch.Generator(device="cuda").manual_seed(seed)
     pages_per = [(s + n + pt - 1) // pt for s, n in reqs]
-    n_pages = sum(pages_per)
+    n_pages = sum(pages_per) + 2
     pool = _pool(n_pages, L, H, D, pt, g)
+    order = (torch.randperm(n_pages, generator=torch.Generator().manual_seed(3)).tolist()
+             if scatter else list(range(n_pages)))
     bt, slices, off = [], [], 0
     for (s, n), np_ in zip(reqs, pages_per):
         slices.append((s, n, off, np_, 1))
-        bt.extend(range(off, off + np_))
+        bt.extend(order[off:off + np_])
         off += np_
     n_tok = sum(n for _, n in reqs)
-    qkv = torch.randn(n_tok, 3 * H * D, device="cuda", generator=g).bfloat16()
-    layer = 1
-    o = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bt, pt)
-    torch.cuda.synchronize()
-    row = 0
+    qkv = torch.randn(n_tok, 3 * H * D, device="cuda", generator=g)
+    qkv[:, :H * D] *= Q_SHARPEN
+    return pool, bt, slices, qkv.bfloat16(), order[off:]
+
+
+def _check_chunk(o, qkv, pool, bt, slices, layer, H, D, pt, negative=True):
+    row, worst = 0, (0.0, 1.0)
     for (s, n, bto, np_, _) in slices:
         K, V = _gather_kv(pool, layer, bt[bto:bto + np_], s + n, pt)
         q = qkv[row:row + n, :H * D].float().view(n, H, D).transpose(0, 1)  # H, n, D
-        sc = torch.einsum("hqd,hkd->hqk", q, K) * D ** -0.5
-        qpos = torch.arange(s, s + n, device="cuda")[:, None]
-        kpos = torch.arange(0, s + n, device="cuda")[None, :]
-        sc = sc.masked_fill(kpos > qpos, float("-inf"))
-        ref = torch.einsum("hqk,hkd->hqd", torch.softmax(sc, -1), V).transpose(0, 1).reshape(n, H * D)
-        err = (o[row:row + n].float() - ref).abs().max().item()
-        assert err < 2e-2, (s, n, err)
+        qpos = torch.arange(s, s + n, device="cuda")
+        ref = _ref_attention(q, K, V, qpos, D ** -0.5).transpose(0, 1)  # n, H, D
+        got = o[row:row + n].view(n, H, D)
+        m = _attn_metric(got, ref)
+        worst = (max(worst[0], m[0]), min(worst[1], m[1]))
+        assert _attn_ok(m), (s, n, m)
+        if negative:  # a causal mask off by one either way must be detected
+            for shift in (-1, 1):
+                bad = _ref_attention(q, K, V, qpos, D ** -0.5, shift).transpose(0, 1)
+                assert not _attn_ok(_attn_metric(got, bad)), (s, n, shift)
         row += n
+    return worst
 
 
-@pytest.mark.parametrize("prefix,n,H", [(0, 512, 40), (3000, 512, 40), (7680, 512, 8),
-                                        (130, 77, 40), (256, 300, 3)])
-def test_chunk_attention_long_prefix_pieces(prefix, n, H):
-    """One slice over a long paged prefix: the stream-K plan cuts (head, tile pair)
-    work into pieces merged by the combine kernel; unaligned starts and lone tiles."""
-    g = torch.Generator(device="cuda").manual_seed(prefix + n)
-    L, D, pt = 2, 128, 16
-    n_pages = (prefix + n + pt - 1) // pt
-    pool = _pool(n_pages, L, H, D, pt, g)
-    bt = torch.randperm(n_pages, generator=torch.Generator().manual_seed(3)).tolist()
-    slices = [(prefix, n, 0, n_pages, 1)]
-    qkv = torch.randn(n, 3 * H * D, device="cuda", generator=g).bfloat16()
-    o = native.chunk_attention(qkv, 3 * H * D, pool, 0, L, H, D, slices, bt, pt)
+def test_chunk_attention_mixed_slices():
+    """A chunk holding a prompt tail with a long prefix, two whole prompts and the
+    head of a fourth prompt (several slices per chunk, as pdsim chunkify packs)."""
+    L, H, D, pt, layer = 2, 4, 128, 16, 1
+    reqs = [(394, 118), (0, 18), (0, 100), (0, 276)]
+    pool, bt, slices, qkv, spare = _chunk_case(reqs, H, 5, L, D, pt)
+    o = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bt, pt)
     torch.cuda.synchronize()
-    heads = sorted({0, H // 2, H - 1})
-    K, V = _gather_kv(pool, 0, bt, prefix + n, pt)
-    q = qkv[:, :H * D].float().view(n, H, D).transpose(0, 1)
-    qpos = torch.arange(prefix, prefix + n, device="cuda")[:, None]
-    kpos = torch.arange(0, prefix + n, device="cuda")[None, :]
-    for h in heads:
-        sc = (q[h] @ K[h].t()) * D ** -0.5
-        sc = sc.masked_fill(kpos > qpos, float("-inf"))
-        ref = torch.softmax(sc, -1) @ V[h]
-        err = (o[:, h * D:(h + 1) * D].float() - ref).abs().max().item()
-        assert err < 2e-2, (h, err)
+    worst = _check_chunk(o, qkv, pool, bt, slices, layer, H, D, pt)
+    # negative control on the device: one prefix page of the first slice swapped
+    bad_bt = list(bt)
+    bad_bt[3] = spare[0]
+    o_bad = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bad_bt, pt)
+    with pytest.raises(AssertionError):
+        _check_chunk(o_bad, qkv, pool, bt, slices[:1], layer, H, D, pt, negative=False)
+    print(f"chunk attention mixed: max rel {worst[0]:.2e}, min cos {worst[1]:.6f}")
+
+
+@pytest.mark.parametrize("prefix,n,H", [(0, 512, 40), (2048, 512, 40), (3000, 512, 40),
+                                        (4096, 512, 40), (7680, 512, 8), (130, 77, 40),
+                                        (256, 300, 3)])
+def test_chunk_attention_long_prefix_pieces(prefix, n, H):
+    """One slice over a long paged prefix (the C2 regime: 2k-8k prompts in 512
+    chunks): the stream-K plan cuts (head, tile pair) work into pieces merged by
+    the combine kernel; unaligned starts and lone tiles.  Every head is checked,
+    with negative controls (shifted mask, and a dropped 128-key block on the
+    device)."""
+    L, D, pt, layer = 2, 128, 16, 0
+    pool, bt, slices, qkv, spare = _chunk_case([(prefix, n)], H, prefix + n, L, D, pt)
+    o = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bt, pt)
+    torch.cuda.synchronize()
+    worst = _check_chunk(o, qkv, pool, bt, slices, layer, H, D, pt)
+    if prefix >= 256:
+        # a whole 128-key block (8 pages) of the prefix replaced by other pages
+        bad_bt = list(bt)
+        for i in range(8):
+            bad_bt[(prefix // 2) // pt + i] = spare[i % len(spare)] if spare else bt[0]
+        o_bad = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bad_bt, pt)
+        with pytest.raises(AssertionError):
+            _check_chunk(o_bad, qkv, pool, bt, slices, layer, H, D, pt, negative=False)
+    print(f"chunk attention prefix {prefix} n {n} H {H}: max rel {worst[0]:.2e}, "
+          f"min cos {worst[1]:.6f}")
 
 
 def test_gemm_shared_workspace_across_shapes():

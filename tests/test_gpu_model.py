@@ -1,11 +1,11 @@
 """End-to-end device parity through the C ABI (tk_prefill_chunk,
 tk_decode_step, tk_kv_send, tk_predict) against the fp32 oracle.
 
-Tolerance (bf16 path vs fp32 oracle): logits agree to within 3% of the
-row's logit range (max |diff| <= 0.03 * (max - min) of the oracle row) and
-cosine similarity >= 0.999; greedy tokens must be identical wherever the
-oracle's top-1/top-2 margin exceeds that bound (near-ties are excluded, as
-SURVEY.md §7 prescribes for random weights).  KV handoff is bit-exact.
+Tolerance (bf16 path vs fp32 oracle): tests/parity_util.py -- logits within
+1% of the row's logit range, cosine >= 0.9999, greedy tokens identical on
+every row whose oracle top-1/top-2 margin exceeds that bound and within the
+tie band on the others (near-ties are expected with random
+weights), with a minimum number of decided rows.  KV handoff is bit-exact.
 """
 
 import numpy as np
@@ -16,6 +16,7 @@ from oracle.model_ref import ARCH_LLAMA, ARCH_OPT, OracleModel, PagedCache, Shap
 from paper_2401_11181_b200 import native
 from paper_2401_11181_b200.prefill import chunkify
 from paper_2401_11181_b200.workload import Request, token_ids_for
+from parity_util import greedy_agrees, logits_close, record
 
 pytestmark = pytest.mark.gpu
 
@@ -28,19 +29,11 @@ def _oshape(m: native.ModelShape) -> Shape:
 
 
 def _close(got: torch.Tensor, ref: torch.Tensor):
-    span = (ref.max(-1).values - ref.min(-1).values).clamp_min(1e-6)
-    err = ((got - ref).abs().max(-1).values / span).max().item()
-    cos = torch.nn.functional.cosine_similarity(got, ref, dim=-1).min().item()
-    assert err <= 0.03 and cos >= 0.999, (err, cos)
-    return err
+    return logits_close(got, ref)[0]
 
 
 def _greedy_agrees(got: torch.Tensor, ref: torch.Tensor):
-    top2 = ref.topk(2, dim=-1)
-    span = ref.max(-1).values - ref.min(-1).values
-    decided = (top2.values[:, 0] - top2.values[:, 1]) > 0.03 * span
-    assert (got.argmax(-1)[decided] == ref.argmax(-1)[decided]).all()
-    return int(decided.sum())
+    return greedy_agrees(got, ref)
 
 
 def _plan(lens, chunk_size):
@@ -54,14 +47,17 @@ def _plan(lens, chunk_size):
 
 
 @pytest.mark.parametrize("model", [native.TINY_OPT, native.TINY_LLAMA])
-def test_prefill_and_decode_match_oracle(model):
-    lens = [18, 100, 512 + 7, 900, 5]
+@pytest.mark.parametrize("lens", [[18, 100, 512, 900], [18, 100, 512 + 7, 900, 5]])
+def test_prefill_and_decode_match_oracle(model, lens):
+    """The reference's prompt lengths (pkg/tests/test_prefill.py:58-67) and a
+    ragged variant whose tail chunk holds two slices."""
     reqs, tables, n_pages, chunks = _plan(lens, 512)
     inst = native.Instance(model, device=0, seed=3, kv_pages=n_pages, page_tokens=PT, max_chunk=512)
     ora = OracleModel.from_instance(_oshape(model), inst)
     cache = PagedCache(ora.s, n_pages, PT)
     prompts = {r.id: token_ids_for(r, model.vocab, seed=11) for r in reqs}
     first_dev, first_ref = {}, {}
+    errs, decided, rows = [], 0, 0
     for chunk in chunks:
         ids, slices, bt = [], [], []
         for rid, start, n in chunk.slices:
@@ -73,8 +69,9 @@ def test_prefill_and_decode_match_oracle(model):
         ref = ora.prefill_chunk(cache, ids, slices, bt)
         emitting = [rid for rid, s, n in chunk.slices if s + n == lens[rid]]
         if emitting:
-            _close(torch.from_numpy(logits), ref)
-            _greedy_agrees(torch.from_numpy(logits), ref)
+            errs.append(_close(torch.from_numpy(logits), ref))
+            decided += _greedy_agrees(torch.from_numpy(logits), ref)
+            rows += len(emitting)
             for (rid, s, n), t in zip(chunk.slices, list(toks)):
                 if s + n == lens[rid]:
                     assert t == int(np.argmax(logits[emitting.index(rid)]))
@@ -96,11 +93,14 @@ def test_prefill_and_decode_match_oracle(model):
         ev, toks, logits = inst.decode_step(last, ctx, bt, stride, want_logits=True)
         ev.wait()
         ref = ora.decode_step(cache, last, ctx, [tables[i] for i in range(len(lens))])
-        _close(torch.from_numpy(logits), ref)
-        _greedy_agrees(torch.from_numpy(logits), ref)
+        errs.append(_close(torch.from_numpy(logits), ref))
+        decided += _greedy_agrees(torch.from_numpy(logits), ref)
+        rows += len(lens)
         assert list(toks) == [int(v) for v in np.argmax(logits, axis=1)]
         last = [int(v) for v in ref.argmax(-1)]
         ctx = [c + 1 for c in ctx]
+    record(f"{model.name}_{len(lens)}prompts", max_err=max(errs), decided=decided, rows=rows)
+    assert decided >= rows // 2, (decided, rows)
     inst.close()
 
 
@@ -152,12 +152,12 @@ def test_predictor_classifier_matches_oracle():
     ev, buckets = inst.predict(sum(prompts, []), lens, max_len=512)
     ev.wait()
     ref = torch.stack([ora.full_forward(p)[-1] for p in prompts])
-    top2 = ref.topk(2, -1)
-    span = ref.max(-1).values - ref.min(-1).values
-    for i in range(len(lens)):
-        if top2.values[i, 0] - top2.values[i, 1] > 0.03 * span[i]:
-            assert buckets[i] == int(ref[i].argmax())
+    b2, scores = inst.predict_scores(sum(prompts, []), lens, max_len=512)
+    assert list(buckets) == b2
+    err = _close(torch.from_numpy(scores), ref)
+    _greedy_agrees(torch.from_numpy(scores), ref)
     assert all(0 <= b < 41 for b in buckets)
+    record("predictor_small", max_err=err)
     inst.close()
 
 
