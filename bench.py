@@ -301,34 +301,51 @@ def run_ours(args, world, rank, local):
         plan, pages = round_plan(batch, chunks, shape.vocab, args.seed)
         plans.append(plan)
         max_pages = max(max_pages, pages)
-    inst = native.Instance(shape, device=local, seed=args.seed, kv_pages=max_pages,
-                           page_tokens=PAGE, max_chunk=CHUNK)
+    # torchrun: one replica per rank on its LOCAL_RANK device.  A plain
+    # ``python bench.py --gpus N``: one process drives N replicas (devices 0..N-1),
+    # issuing every round's chunks to all of them before waiting on any.
+    if world == 1 and args.gpus > 1:
+        n_dev = native.device_count()
+        if n_dev < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {n_dev} CUDA device(s) visible")
+        devs = list(range(args.gpus))
+    else:
+        devs = [local]
+    insts = [native.Instance(shape, device=d, seed=args.seed, kv_pages=max_pages,
+                             page_tokens=PAGE, max_chunk=CHUNK) for d in devs]
+    inst = insts[0]
 
-    def run_round(plan):
-        evs, toks = [], 0
-        h2d = d2h = 0
+    def run_round(plan, which=None):
+        which = insts if which is None else which
+        evs = [[] for _ in which]
+        toks = h2d = d2h = 0
         verbose = os.environ.get("TK_BENCH_VERBOSE")
         for ci, (ids, slices, bt, real) in enumerate(plan):
-            ev, out = inst.prefill_chunk(ids, slices, bt)
-            if verbose:
-                ev.wait()
-                print(f"chunk {ci} slices={[(s[0], s[1]) for s in slices]} "
-                      f"{ev.elapsed_ns / 1e6:.2f} ms", file=sys.stderr, flush=True)
-            a, b = inst.staged_bytes()
-            h2d, d2h = h2d + a, d2h + b
-            evs.append((ev, out))
-            toks += real
-        for ev, _ in evs:
-            ev.wait()  # publishes each chunk's first tokens to host memory
-        dev_ns = native.event_elapsed_ns(evs[0][0], evs[-1][0])
+            for k, ins in enumerate(which):
+                ev, out = ins.prefill_chunk(ids, slices, bt)
+                if verbose:
+                    ev.wait()
+                    print(f"dev {ins.device} chunk {ci} slices={[(s[0], s[1]) for s in slices]} "
+                          f"{ev.elapsed_ns / 1e6:.2f} ms", file=sys.stderr, flush=True)
+                a, b = ins.staged_bytes()
+                h2d, d2h = h2d + a, d2h + b
+                evs[k].append((ev, out))
+                toks += real
+        for per in evs:
+            for ev, _ in per:
+                ev.wait()  # publishes each chunk's first tokens to host memory
+        # device time of the slowest replica (max over devices)
+        dev_ns = max(native.event_elapsed_ns(per[0][0], per[-1][0]) for per in evs)
         return toks, dev_ns, h2d, d2h
 
     for i in range(args.warmup):
         run_round(plans[i % len(plans)])
-    inst.sync()
-    clocks = ClockSampler(local)
+    for ins in insts:
+        ins.sync()
+    clocks = ClockSampler(local if len(devs) == 1 else ",".join(map(str, devs)))
     barrier(world)
-    inst.sync()
+    for ins in insts:
+        ins.sync()
     clocks.start()
     launches0 = native.launch_count()
     t0 = time.perf_counter()
@@ -336,25 +353,27 @@ def run_ours(args, world, rank, local):
     for i in range(args.steps):
         t, ns, a, b = run_round(plans[(args.warmup + i) % len(plans)])
         tokens, dev_ns, h2d, d2h = tokens + t, dev_ns + ns, h2d + a, d2h + b
-    inst.sync()
+    for ins in insts:
+        ins.sync()
     wall = time.perf_counter() - t0
     launches = native.launch_count() - launches0
     barrier(world)
     clk = clocks.stop()
-    # Per-kernel breakdown (roofline, shares): the same rounds again, every
-    # launch bracketed by CUDA events on the compute stream.  Kept out of the
-    # timed region above so the event records do not perturb `value`.
+    # Per-kernel breakdown (roofline, shares): the same rounds again on the first
+    # replica, every launch bracketed by CUDA events on the compute stream.  Kept
+    # out of the timed region above so the event records do not perturb `value`.
     inst.profile(True)
     prof_ns = 0
     for i in range(args.steps):
-        prof_ns += run_round(plans[(args.warmup + i) % len(plans)])[1]
+        prof_ns += run_round(plans[(args.warmup + i) % len(plans)], [inst])[1]
     inst.sync()
     prof = inst.profile_read()
     inst.profile(False)
 
     dev_s = dist_max(dev_ns / 1e9, world)
     wall_s = dist_max(wall, world)
-    total_tokens = tokens * world
+    total_tokens = tokens * world  # tokens already counts every replica of this process
+    n_gpus = world * len(devs)
     peaks = measured_peaks()
     gemm_kinds = ("qkv_gemm", "o_gemm", "fc1_gemm", "fc2_gemm")
     g_ms = sum(prof[k]["ms"] for k in gemm_kinds)
@@ -364,13 +383,17 @@ def run_ours(args, world, rank, local):
     traffic = gemm_traffic(prof)
     peak = peaks["bf16_tflops_sustained"]
     attn = prof["attention"]
+    for ins in insts[1:]:
+        ins.close()
     if rank != 0:
+        inst.close()
+        barrier(world)  # rank 0 runs the cross-GPU legs once every replica is closed
         return
     line = {
         "metric": METRIC,
         "value": round(total_tokens / dev_s, 2),
         "unit": "tok/s",
-        "n_gpus": world,
+        "n_gpus": n_gpus,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(dev_s / args.steps * 1e3, 3),
@@ -386,7 +409,9 @@ def run_ours(args, world, rank, local):
             "model": shape.name, "chunk_size": CHUNK, "page_tokens": PAGE,
             "step": "one scheduling round (16 prompts, all chunks, first tokens read back)",
             "tokens_per_step": tokens // max(1, args.steps),
-            "parallelism": f"replicas x{world} (weak)",
+            "parallelism": (f"prefill replicas x{n_gpus} (weak; "
+                            + ("torchrun, one rank per GPU" if world > 1 else
+                               "one process driving every GPU") + ")"),
             "l2": "inputs larger than L2 (25.8 GB of weights streamed per chunk)",
         },
         "e2e": {"value": round(total_tokens / wall_s, 2), "unit": "tok/s",
@@ -410,18 +435,22 @@ def run_ours(args, world, rank, local):
     }
     line["share_of_step"] = {k: round(v["ms"] / (prof_ns / 1e6), 4) for k, v in prof.items()}
     inst.close()
-    if world == 1 and not args.no_decode:
+    if n_gpus > 1:
+        barrier(world)  # every other rank has closed its replica
+        line["multi_gpu"] = guarded(lambda: multi_gpu_run(args, n_gpus, peaks))
+    if n_gpus == 1 and not args.no_decode:
         line["decode"] = decode_run(args, shape, local, peaks)
         if args.model == "opt-13b":
             # BASELINE.json configs[4] at one GPU: Llama-2-7B-shaped large decode batches
             line["decode"].update(decode_run(args, native.MODELS["llama-2-7b"], local, peaks,
                                              configs=((256, 1024),), tag="llama-2-7b_"))
-    if world == 1 and not args.no_decode:
-        line["kv_handoff"] = handoff_run(args, shape, local, peaks)
+    if n_gpus == 1 and not args.no_decode:
+        line["kv_handoff"] = guarded(lambda: handoff_run(args, shape, local, local, peaks))
+        line["kv_handoff"]["overlap"] = guarded(lambda: overlap_run(args, shape, local, local))
         line["predictor"] = predictor_run(args, local, peaks)
-    if world == 1 and not args.no_serving:
+    if n_gpus == 1 and not args.no_serving:
         line["serving"] = serving_run(args)
-    if world == 1 and not args.no_cpu_baseline:
+    if n_gpus == 1 and not args.no_cpu_baseline:
         all_chunks = [(p[1], p[3]) for plan in plans for p in plan]
         pick = [all_chunks[int(i * len(all_chunks) / 6)] for i in range(6)]
         tok_s, cores, desc = cpu_port_sample(pick, max_seconds=args.cpu_seconds)
@@ -473,41 +502,155 @@ def decode_run(args, shape, device: int, peaks: dict, configs=((32, 2048), (128,
     return out
 
 
-def handoff_run(args, shape, device: int, peaks: dict, prompts=(512, 900, 8192)) -> dict:
-    """P->D KV handoff (tk_kv_send, pdsim/prefill.py:420-424) between two
-    instances co-located on one GPU: one copy-kernel launch per request, pages
-    scattered on both sides.  bytes = prompt pages x page bytes (costs.py:137
-    rounds to whole pages here); HBM traffic = 2 x bytes (read + write)."""
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (spec)
+
+
+def p2p_copy_gbs(src: int, dst: int, nbytes: int = 1 << 30) -> float:
+    """Measured device->peer copy bandwidth (torch copy over NVLink, best of 5,
+    CUDA events on the source): the achievable figure beside the 900 GB/s spec."""
+    import torch
+    a = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{src}")
+    b = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dst}")
+    best = 0.0
+    with torch.cuda.device(src):
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b.copy_(a, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del a, b
+    torch.cuda.empty_cache()
+    return best
+
+
+def handoff_run(args, shape, src_dev: int, dst_dev: int, peaks: dict,
+                prompts=(512, 900, 8192), engines=("sm", "ce"), p2p_gbs: float | None = None) -> dict:
+    """P->D KV handoff (tk_kv_send_ex, pdsim/prefill.py:420-424): one request's
+    prompt pages, scattered on both sides, from an instance on ``src_dev`` to one
+    on ``dst_dev``.  bytes = prompt pages x page bytes (costs.py:137 rounds to
+    whole pages here).  Co-located (same device): HBM-bound, traffic 2 x bytes.
+    Across devices: NVLink-bound, against 900 GB/s per direction (spec) and the
+    measured peer copy bandwidth.  Engines: "sm" = the page-copy kernel (peer
+    stores), "ce" = copy engines."""
     import random
 
     from paper_2401_11181_b200 import costs, native
     n_max = (max(prompts) + PAGE - 1) // PAGE
-    src = native.Instance(shape, device=device, seed=args.seed, kv_pages=n_max + 64, max_chunk=64)
-    dst = native.Instance(shape, device=device, seed=args.seed, kv_pages=n_max + 64, max_chunk=64)
+    src = native.Instance(shape, device=src_dev, seed=args.seed, kv_pages=n_max + 64, max_chunk=64)
+    dst = native.Instance(shape, device=dst_dev, seed=args.seed, kv_pages=n_max + 64, max_chunk=64)
     rng = random.Random(args.seed)
-    out = {"note": "single GPU: device-local copy bounded by HBM; NVLink peer stores use the "
-                   "same kernel with a peer destination pool (not measurable on a 1-GPU box)"}
-    for n_tok in prompts:
-        n = (n_tok + PAGE - 1) // PAGE
-        sp, dp = rng.sample(range(n_max + 64), n), rng.sample(range(n_max + 64), n)
-        for _ in range(3):
-            src.kv_send(sp, dst, dp).wait()
-        evs = [src.kv_send(sp, dst, dp) for _ in range(8)]
-        for e in evs:
-            e.wait()
-        ns = sorted(e.elapsed_ns for e in evs)[len(evs) // 2]
-        nbytes = n * src.page_bytes
-        hbm = 2 * nbytes / (ns / 1e9) / 1e9
-        out[f"prompt{n_tok}"] = {
-            "pages": n, "bytes": nbytes, "device_us": round(ns / 1e3, 1),
-            "handoff_gb_s": round(nbytes / (ns / 1e9) / 1e9, 1),
-            "roofline": {"bound": "hbm", "achieved": round(hbm, 1), "peak": peaks["hbm_gbs"],
-                         "unit": "GB/s", "frac": round(hbm / peaks["hbm_gbs"], 4)},
-            "reference_modeled_us_nvlink300": costs.transfer_latency(
-                costs.load_calibration({"preset": "nvlink300"}), n_tok),
-        }
+    local = src_dev == dst_dev
+    out = {"src_device": src_dev, "dst_device": dst_dev,
+           "link": "device-local copy (co-located P and D), HBM-bound" if local else
+                   "NVLink 5 / NVSwitch peer path"}
+    if not local and p2p_gbs:
+        out["p2p_copy_gbs_measured"] = round(p2p_gbs, 1)
+    for engine in engines:
+        res = {}
+        for n_tok in prompts:
+            n = (n_tok + PAGE - 1) // PAGE
+            sp, dp = rng.sample(range(n_max + 64), n), rng.sample(range(n_max + 64), n)
+            for _ in range(3):
+                src.kv_send(sp, dst, dp, engine).wait()
+            evs = [src.kv_send(sp, dst, dp, engine) for _ in range(8)]
+            for e in evs:
+                e.wait()
+            ns = sorted(e.elapsed_ns for e in evs)[len(evs) // 2]
+            nbytes = n * src.page_bytes
+            gbs = nbytes / (ns / 1e9) / 1e9
+            r = {"pages": n, "bytes": nbytes, "device_us": round(ns / 1e3, 1),
+                 "handoff_gb_s": round(gbs, 1),
+                 "reference_modeled_us_nvlink300": costs.transfer_latency(
+                     costs.load_calibration({"preset": "nvlink300"}), n_tok)}
+            if local:
+                hbm = 2 * gbs
+                r["roofline"] = {"bound": "hbm", "achieved": round(hbm, 1),
+                                 "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                 "frac": round(hbm / peaks["hbm_gbs"], 4)}
+            else:
+                r["roofline"] = {"bound": "nvlink", "achieved": round(gbs, 1),
+                                 "peak": NVLINK_GBS, "unit": "GB/s",
+                                 "frac": round(gbs / NVLINK_GBS, 4)}
+                if p2p_gbs:
+                    r["roofline"]["frac_of_measured_p2p"] = round(gbs / p2p_gbs, 4)
+            res[f"prompt{n_tok}"] = r
+        out[engine] = res
     src.close(), dst.close()
     return out
+
+
+def overlap_run(args, shape, src_dev: int, dst_dev: int, prefix: int = 4096,
+                send_tokens: int = 8192, engines=("sm", "ce"), reps: int = 5) -> dict:
+    """Handoff/compute overlap (pdsim/prefill.py:420-424: sends run free beside
+    the next chunk).  One 512-token chunk at a ``prefix``-token prefix on the
+    prefill instance, alone and with a ``send_tokens``-token request's handoff
+    issued right before it (the send waits for the previous chunk, then runs
+    on the copy stream while this chunk computes).  Reported per engine: chunk
+    time alone / under the send, send time alone / under the chunk, and the
+    overlap efficiency (alone chunk + alone send) / concurrent makespan."""
+    import random
+    import statistics as st
+
+    from paper_2401_11181_b200 import native
+    from paper_2401_11181_b200.workload import Request, token_ids_for
+    n_req = (prefix + CHUNK + PAGE - 1) // PAGE
+    n_send = (send_tokens + PAGE - 1) // PAGE
+    src = native.Instance(shape, device=src_dev, seed=args.seed, kv_pages=n_req + n_send,
+                          page_tokens=PAGE, max_chunk=CHUNK)
+    dst = native.Instance(shape, device=dst_dev, seed=args.seed, kv_pages=n_send,
+                          page_tokens=PAGE, max_chunk=64)
+    req = Request(id=0, arrival_us=0, prompt_len=prefix + CHUNK, true_decode_len=1)
+    ids = token_ids_for(req, shape.vocab, args.seed)
+    bt = list(range(n_req))
+    for c0 in range(0, prefix, CHUNK):  # fill the prefix KV once
+        src.prefill_chunk(ids[c0:c0 + CHUNK], [(c0, CHUNK, 0, n_req, 0)], bt)[0].wait()
+    chunk = (ids[prefix:], [(prefix, CHUNK, 0, n_req, 1)], bt)
+    rng = random.Random(args.seed)
+    sp = [n_req + i for i in rng.sample(range(n_send), n_send)]
+    dp = rng.sample(range(n_send), n_send)
+    for _ in range(2):
+        src.prefill_chunk(*chunk)[0].wait()
+    alone = []
+    for _ in range(reps):
+        alone.append(src.prefill_chunk(*chunk)[0].wait())
+    out = {"chunk": f"512 tokens at prefix {prefix} ({shape.name})",
+           "send": f"{send_tokens}-token request ({n_send} pages, {n_send * src.page_bytes} B)",
+           "devices": [src_dev, dst_dev], "chunk_alone_us": round(st.median(alone) / 1e3, 1)}
+    for engine in engines:
+        s_alone, c_under, s_under, span = [], [], [], []
+        for _ in range(reps):
+            s_alone.append(src.kv_send(sp, dst, dp, engine).wait())
+        for _ in range(reps):
+            src.prefill_chunk(*chunk)[0].wait()
+            pre = src.prefill_chunk(*chunk)[0]          # chunk k
+            sev = src.kv_send(sp, dst, dp, engine)      # its handoff, after chunk k
+            cev = src.prefill_chunk(*chunk)[0]          # chunk k+1, concurrent with the send
+            c_under.append(cev.wait())
+            s_under.append(sev.wait())
+            pre.wait()
+            span.append(max(native.event_elapsed_ns(sev, cev), native.event_elapsed_ns(sev, sev)))
+        ca, sa = st.median(alone), st.median(s_alone)
+        mk = st.median(span)
+        out[engine] = {"send_alone_us": round(sa / 1e3, 1),
+                       "chunk_under_send_us": round(st.median(c_under) / 1e3, 1),
+                       "send_under_chunk_us": round(st.median(s_under) / 1e3, 1),
+                       "makespan_us": round(mk / 1e3, 1),
+                       "chunk_slowdown": round(st.median(c_under) / ca, 4),
+                       "overlap_efficiency": round((ca + sa) / mk, 4)}
+    src.close(), dst.close()
+    return out
+
+
+def guarded(fn):
+    """Run an auxiliary leg; a failure is recorded in the line instead of losing it."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001 -- reported, never hidden
+        import traceback
+        traceback.print_exc()
+        return {"error": f"{type(e).__name__}: {e}"[:400]}
 
 
 def predictor_run(args, device: int, peaks: dict, n: int = 16, length: int = 512) -> dict:
@@ -534,46 +677,134 @@ def predictor_run(args, device: int, peaks: dict, n: int = 16, length: int = 512
             "note": "tiny model: launch/latency bound, not tensor bound"}
 
 
-def serving_run(args) -> dict:
-    """Mixed workload through the reference scheduler + CUDA executor (measured clock)."""
+C3_MIX = {"LPLD": 0.5, "HPLD": 0.5}     # summarization-like (BASELINE configs[2])
+C5_MIX = {"LPHD": 0.5, "HPHD": 0.5}     # content creation (BASELINE configs[4])
+
+
+def serving_leg(args, n_prefill: int, n_decode: int, n_requests: int, mixture: dict | None = None,
+                model: str | None = None, colocate: bool = False, coupled: bool = False,
+                streaming: bool = False, capacity_tokens: int | None = None) -> dict:
+    """One serving run through the reference scheduler + CUDA executor (real
+    clock, completion stamps = CUDA-event times) on GPUs 0.. (p{i} then d{j}),
+    or every instance on GPU 0 when ``colocate``, beside the same workload on the modeled clock (pdsim's V100 cost
+    model through this package's bit-identical port; its single-thread wall time
+    is the CPU baseline of the scheduler)."""
     import paper_2401_11181_b200 as tk
+    from paper_2401_11181_b200 import native
     from paper_2401_11181_b200.experiment import run_experiment
-    cfg = {"cluster": {"prefill": 1, "decode": 1},
-           "workload": {"n_requests": args.serving_n},
-           "cost_model": {"preset": "nvlink300", "mem_capacity_tokens": 40000},
-           "model": {"name": args.model, "prefill_pages": 2048, "staging_pages": 512,
-                     "max_decode_batch": 256, "seed": args.seed}}
-    sim = run_experiment(tk.config_from_dict(cfg), seed=args.seed).summary
-    res = run_experiment(tk.config_from_dict(dict(cfg, executor="cuda")), seed=args.seed)
+    model = model or args.model
+    shape = native.MODELS[model]
+    n_gpus = 1 if colocate else n_prefill + n_decode
+    if n_gpus > native.device_count():
+        raise RuntimeError(f"{n_prefill}P:{n_decode}D needs {n_gpus} GPUs, "
+                           f"{native.device_count()} visible")
+    wl = {"n_requests": n_requests}
+    if mixture:
+        wl["mixture"] = dict(mixture)
+    cm = {"preset": "nvlink300", "kv_bytes_per_token": shape.kv_bytes_per_token}
+    if capacity_tokens:
+        cm["mem_capacity_tokens"] = capacity_tokens
+    mcfg = {"name": model, "prefill_pages": 2048, "staging_pages": 512,
+            "max_decode_batch": 256, "seed": args.seed}
+    if capacity_tokens is None:
+        mcfg["capacity_from_hbm"] = True
+    devices = {}
+    if not coupled:
+        devices.update({f"p{i}": i for i in range(n_prefill)})
+        devices.update({f"d{j}": n_prefill + j for j in range(n_decode)})
+        cluster = {"prefill": n_prefill, "decode": n_decode}
+    else:
+        cluster = {"coupled": n_prefill}
+        devices.update({f"c{i}": i for i in range(n_prefill)})
+    if colocate:
+        devices = {k: 0 for k in devices}
+    cfg = {"cluster": cluster, "workload": wl, "cost_model": cm, "model": mcfg,
+           "devices": devices}
+    if coupled:
+        cfg["system"] = "coupled"
+    t0 = time.perf_counter()
+    sim = run_experiment(tk.config_from_dict(dict(cfg, model={k: v for k, v in mcfg.items()
+                                                               if k != "capacity_from_hbm"})),
+                         seed=args.seed).summary
+    sim_wall = time.perf_counter() - t0
+    dev_cfg = dict(cfg, executor="cuda")
+    if streaming:
+        dev_cfg["kv_streaming"] = "chunk"
+    res = run_experiment(tk.config_from_dict(dev_cfg), seed=args.seed)
     s, d = res.summary, res.summary["device"]
-    st = run_experiment(tk.config_from_dict(dict(cfg, executor="cuda", kv_streaming="chunk")),
-                        seed=args.seed).summary
-    coupled_cfg = dict(cfg, system="coupled", cluster={"coupled": 1}, executor="cuda")
-    c = run_experiment(tk.config_from_dict(coupled_cfg), seed=args.seed).summary
-    return {
-        "workload": f"Mixed-{args.serving_n} (four-class, burst), 1 prefill + 1 decode instance "
-                    f"co-located on one GPU, {args.model}, reserve_dynamic, power-of-two, "
-                    "predictor g=200 p=0.749 (device classifier for cost)",
+    gen_tokens = sum(r["decode_len"] for r in res.rows)
+    prompt_tokens = sum(r["prompt_len"] for r in res.rows)
+    phys = d.get("gpus_used", n_gpus)
+    out = {
+        "system": "coupled" if coupled else "tetriinfer",
+        "split": f"{n_prefill}C" if coupled else f"{n_prefill}P:{n_decode}D",
+        "gpus": phys, "model": model, "n_requests": n_requests,
+        "mixture": mixture or "DEFAULT_MIXTURE (uniform four-class)",
         "ttft_avg_ms": round(s["ttft"]["avg_us"] / 1e3, 2),
         "jct_avg_ms": round(s["jct"]["avg_us"] / 1e3, 2),
         "ttft_p99_ms": round(s["ttft"]["p99_us"] / 1e3, 2),
         "jct_p99_ms": round(s["jct"]["p99_us"] / 1e3, 2),
-        "prefill_tok_s": round(d.get("prefill_tok_s_device", 0.0), 1),
-        "decode_tok_s": round(d.get("decode_tok_s_device", 0.0), 1),
-        "kv_handoff_gb_s": round(d.get("handoff_gb_s", 0.0), 1),
         "makespan_s": round(s["makespan_us"] / 1e6, 3),
+        "tok_s_per_gpu": round((gen_tokens + prompt_tokens) / (s["makespan_us"] / 1e6) / phys, 1),
+        "decode_tok_s_per_gpu": round(gen_tokens / (s["makespan_us"] / 1e6) / phys, 1),
+        "prefill_tok_s_device": round(d.get("prefill_tok_s_device", 0.0), 1),
+        "decode_tok_s_device": round(d.get("decode_tok_s_device", 0.0), 1),
+        "kv_handoff_gb_s": round(d.get("handoff_gb_s", 0.0), 1),
+        "decode_capacity_tokens": d.get("mem_capacity_tokens"),
+        "perf_per_dollar": round(s["perf_per_dollar"], 4),
+        "perf_per_dollar_physical": round(d.get("perf_per_dollar_physical", 0.0), 4),
+        "gpu_resource_s": round(d.get("gpu_resource_us", 0) / 1e6, 3),
         "reference_modeled": {"ttft_avg_ms": round(sim["ttft"]["avg_us"] / 1e3, 2),
                               "jct_avg_ms": round(sim["jct"]["avg_us"] / 1e3, 2),
-                              "note": "pdsim cost model (V100-calibrated), same workload"},
-        "coupled_baseline": {"system": "coupled (vLLM-like, pdsim/coupled.py) on the same GPU",
-                             "ttft_avg_ms": round(c["ttft"]["avg_us"] / 1e3, 2),
-                             "jct_avg_ms": round(c["jct"]["avg_us"] / 1e3, 2),
-                             "perf_per_dollar": round(c["perf_per_dollar"], 4)},
-        "perf_per_dollar": round(s["perf_per_dollar"], 4),
-        "kv_streaming_chunk": {"note": "same run with each chunk's KV shipped as it completes",
-                               "ttft_avg_ms": round(st["ttft"]["avg_us"] / 1e3, 2),
-                               "jct_avg_ms": round(st["jct"]["avg_us"] / 1e3, 2)},
+                              "scheduler_wall_s": round(sim_wall, 3),
+                              "note": "pdsim cost model (V100-calibrated) on the same workload; "
+                                      "wall time of the single-thread scheduler port"},
     }
+    if streaming:
+        out["kv_streaming"] = "chunk"
+    return out
+
+
+def serving_run(args) -> dict:
+    """One GPU, co-located instances: Mixed-N (C1/C4 proxy) TetriInfer vs the
+    coupled baseline, and the Llama-2-7B LPHD/HPHD decode-heavy mix (C5 proxy)."""
+    n = args.serving_n
+    out = {"note": "1 GPU: prefill and decode instances co-located (separate streams and "
+                   "pools, device-local KV handoff); perf_per_dollar_physical bills the GPU "
+                   "once, perf_per_dollar is pdsim's sum of instance episode spans"}
+    out[f"mixed{n}_1p1d"] = guarded(lambda: serving_leg(args, 1, 1, n, colocate=True))
+    out[f"mixed{n}_1p1d_streaming"] = guarded(
+        lambda: serving_leg(args, 1, 1, n, colocate=True, streaming=True))
+    out[f"mixed{n}_coupled"] = guarded(lambda: serving_leg(args, 1, 0, n, colocate=True,
+                                                           coupled=True))
+    out["c5proxy_llama_lphd_hphd_1p1d"] = guarded(
+        lambda: serving_leg(args, 1, 1, n, mixture=C5_MIX, model="llama-2-7b", colocate=True))
+    return out
+
+
+def multi_gpu_run(args, n: int, peaks: dict) -> dict:
+    """The disaggregated system on n GPUs of this box (one host process drives
+    every instance; pdsim/control.py's scheduler is centralised):
+    cross-GPU KV handoff over NVLink (SM peer-store kernel vs copy engines),
+    handoff/compute overlap, and P:D-split serving -- C3 (1P:1D, LPLD/HPLD) on 2
+    GPUs, C4 splits 1:3 and 2:2 on 4, 2:6 and 4:4 on 8, C5 (Llama-2-7B,
+    LPHD/HPHD, 2:6) on 8 (BASELINE.json configs[2..4])."""
+    from paper_2401_11181_b200 import native
+    shape = native.MODELS[args.model]
+    out = {"n_gpus": n}
+    p2p = guarded(lambda: p2p_copy_gbs(0, 1))
+    gbs = p2p if isinstance(p2p, float) else None
+    out["kv_handoff_nvlink"] = guarded(lambda: handoff_run(args, shape, 0, 1, peaks, p2p_gbs=gbs))
+    out["overlap_nvlink"] = guarded(lambda: overlap_run(args, shape, 0, 1))
+    legs = {2: [("c3_1p1d", 1, 1, C3_MIX, None)],
+            4: [("c4_1p3d", 1, 3, None, None), ("c4_2p2d", 2, 2, None, None)],
+            8: [("c4_2p6d", 2, 6, None, None), ("c4_4p4d", 4, 4, None, None),
+                ("c5_llama_2p6d", 2, 6, C5_MIX, "llama-2-7b")]}
+    n_req = {"c5_llama_2p6d": args.c5_n}
+    for name, p, d, mix, model in legs.get(n, []):
+        out[name] = guarded(lambda: serving_leg(args, p, d, n_req.get(name, args.serving_multi_n),
+                                                mixture=mix, model=model))
+    return out
 
 
 def main():
@@ -591,7 +822,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-serving", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
-    ap.add_argument("--serving-n", type=int, default=32)
+    ap.add_argument("--serving-n", type=int, default=128)
+    ap.add_argument("--serving-multi-n", type=int, default=128)
+    ap.add_argument("--c5-n", type=int, default=1024)
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -81,6 +81,9 @@ typedef struct tk_event tk_event;
 const char* tk_last_error(void);
 int tk_version(void);
 int tk_device_count(int32_t* n);
+/* Free / total HBM of a device (sizes the decode KV capacity from real free
+ * memory in B200 mode; replaces the constant pdsim/costs.py:46).            */
+int tk_device_memory(int32_t device, int64_t* free_bytes, int64_t* total_bytes);
 
 /* --- instances ------------------------------------------------------------
  * An instance = model weights (shared by every instance of the same model
@@ -127,6 +130,15 @@ int tk_decode_step(tk_instance* inst, int32_t batch, const int32_t* last_tokens,
  * on src's copy stream, ordered after all work already issued on src.        */
 int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
                const int32_t* dst_pages, int32_t n_pages, tk_event** ev);
+/* Same handoff with an explicit engine: TK_SEND_AUTO (= tk_kv_send: the SM
+ * page-copy kernel when src can address dst's pool, else the copy engine),
+ * TK_SEND_SM (kernel on src's SMs: peer stores over NVLink / device copy),
+ * TK_SEND_CE (copy engines: one async copy per run of consecutive pages;
+ * leaves the SMs to the next chunk).  Replaces the same stand-in,
+ * pdsim/costs.py:130-139 (called from pdsim/prefill.py:420-424).             */
+enum { TK_SEND_AUTO = 0, TK_SEND_SM = 1, TK_SEND_CE = 2 };
+int tk_kv_send_ex(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
+                  const int32_t* dst_pages, int32_t n_pages, int32_t engine, tk_event** ev);
 /* Length predictor: sequence classification over n prompts (ids packed,
  * lens[i] each, truncated to max_len), on the predictor stream.  bucket_out[i]
  * = argmax over the instance's n_labels classes.                             */
@@ -158,6 +170,11 @@ int tk_instance_sync(tk_instance* inst);
 /* Device time between the start marker of `a` and the end marker of `b`
  * (both done; same device).                                                 */
 int tk_event_elapsed(tk_event* a, tk_event* b, int64_t* elapsed_ns);
+/* A completed marker on `device`, recorded and synchronized inside the call:
+ * the host reads its own clock on return, and tk_event_elapsed(anchor, ev)
+ * then maps any later event of that device to host time (completion stamps
+ * of TTFT/JCT, pdsim/control.py:334-352, are device times, not poll times). */
+int tk_event_anchor(int32_t device, tk_event** anchor);
 
 /* --- instrumentation --------------------------------------------------------
  * Kernels launched by this library since load (all instances).             */

@@ -170,6 +170,72 @@ __global__ void __launch_bounds__(kNormThreads)
   }
 }
 
+// One WARP per row (4 rows per 128-thread CTA), for cols = 128·PER: lane l owns
+// the float4 groups l, l+32, ...  Every load of the row (x, delta, then w, b) is
+// issued before the first reduction, the reductions are shuffles only (no
+// __syncthreads), and a 512-row chunk is a single wave of 128 CTAs -- the kernel
+// is one DRAM round trip instead of the CTA-per-row kernel's load / barrier /
+// barrier / store sequence.  Same arithmetic order per element as norm_kernel.
+template <bool kRms, bool kAdd, int PER>
+__global__ void __launch_bounds__(128)
+    norm_warp_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+                     const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ b,
+                     __nv_bfloat16* __restrict__ y, int rows, int cols, float eps) {
+  griddep_launch();
+  griddep_wait();
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const size_t row = static_cast<size_t>(r) * cols;
+  float4 v[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) v[k] = *reinterpret_cast<const float4*>(x + row + (lane + 32 * k) * 4);
+  if constexpr (kAdd) {
+    uint2 d[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) d[k] = *reinterpret_cast<const uint2*>(delta + row + (lane + 32 * k) * 4);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const float4 f = bf16x4_to_f4(d[k]);
+      v[k].x += f.x; v[k].y += f.y; v[k].z += f.z; v[k].w += f.w;
+      *reinterpret_cast<float4*>(x + row + (lane + 32 * k) * 4) = v[k];
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  float mean = 0.f;
+  if (!kRms) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    mean = s / cols;
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const float a = v[k].x - mean, bb = v[k].y - mean, cc = v[k].z - mean, dd = v[k].w - mean;
+    ss += (a * a + bb * bb) + (cc * cc + dd * dd);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float rstd = rsqrtf(ss / cols + eps);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = (lane + 32 * k) * 4;
+    const float4 wv = bf16x4_to_f4(__ldg(reinterpret_cast<const uint2*>(w + c)));
+    float4 o = make_float4((v[k].x - mean) * rstd * wv.x, (v[k].y - mean) * rstd * wv.y,
+                           (v[k].z - mean) * rstd * wv.z, (v[k].w - mean) * rstd * wv.w);
+    if (!kRms) {
+      const float4 bv = bf16x4_to_f4(__ldg(reinterpret_cast<const uint2*>(b + c)));
+      o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
+    }
+    uint2 pk;
+    pk.x = pack_bf16x2(o.x, o.y);
+    pk.y = pack_bf16x2(o.z, o.w);
+    *reinterpret_cast<uint2*>(y + row + c) = pk;
+  }
+}
+
 int launch_layernorm(const float* x, const __nv_bfloat16* w, const __nv_bfloat16* b,
                      __nv_bfloat16* y, int rows, int cols, float eps, cudaStream_t s) {
   return launch_add_norm(const_cast<float*>(x), nullptr, w, b, y, rows, cols, eps, false, s);
@@ -187,6 +253,28 @@ int launch_add_norm(float* x, const __nv_bfloat16* delta, const __nv_bfloat16* w
            "norm: cols must be a multiple of 4 and <= 8192");
   if (rows == 0) return TK_OK;
   const __nv_bfloat16* bb = rms ? nullptr : b;
+  if (cols % 128 == 0 && cols <= 128 * 40) {
+    using WFn = void (*)(float*, const __nv_bfloat16*, const __nv_bfloat16*,
+                         const __nv_bfloat16*, __nv_bfloat16*, int, int, float);
+    WFn wk = nullptr;
+#define TK_WNORM_CASE(P)                                                                        \
+  case P:                                                                                       \
+    wk = rms ? (delta ? norm_warp_kernel<true, true, P> : norm_warp_kernel<true, false, P>)     \
+             : (delta ? norm_warp_kernel<false, true, P> : norm_warp_kernel<false, false, P>);  \
+    break;
+    switch (cols / 128) {
+      TK_WNORM_CASE(6) TK_WNORM_CASE(8) TK_WNORM_CASE(16) TK_WNORM_CASE(32) TK_WNORM_CASE(40)
+      TK_WNORM_CASE(2) TK_WNORM_CASE(4)
+      default: break;
+    }
+#undef TK_WNORM_CASE
+    if (wk) {
+      TK_CUDA(launch_pdl(wk, dim3((rows + 3) / 4), dim3(128), 0, s, x, delta, w, bb, y, rows,
+                         cols, eps));
+      note_launch();
+      return TK_OK;
+    }
+  }
   const int per = (cols + kNormThreads * 4 - 1) / (kNormThreads * 4);
   using Fn = void (*)(float*, const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
                       __nv_bfloat16*, int, float);

@@ -961,8 +961,15 @@ int tk_decode_step(tk_instance* inst, int32_t batch, const int32_t* last_tokens,
 // ------------------------------------------------------------------ KV handoff
 int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
                const int32_t* dst_pages, int32_t n_pages, tk_event** ev_out) {
+  return tk_kv_send_ex(src, src_pages, dst, dst_pages, n_pages, TK_SEND_AUTO, ev_out);
+}
+
+int tk_kv_send_ex(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
+                  const int32_t* dst_pages, int32_t n_pages, int32_t engine, tk_event** ev_out) {
   TK_CHECK(src && dst && ev_out && (n_pages == 0 || (src_pages && dst_pages)), TK_EINVAL,
            "tk_kv_send: null argument");
+  TK_CHECK(engine == TK_SEND_AUTO || engine == TK_SEND_SM || engine == TK_SEND_CE, TK_EINVAL,
+           "tk_kv_send: engine must be TK_SEND_AUTO, TK_SEND_SM or TK_SEND_CE");
   TK_CHECK(src->page_bytes == dst->page_bytes, TK_EINVAL, "tk_kv_send: page geometry differs");
   for (int i = 0; i < n_pages; ++i)
     TK_CHECK(src_pages[i] >= 0 && src_pages[i] < src->kv_pages && dst_pages[i] >= 0 &&
@@ -981,7 +988,9 @@ int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
   const int64_t pb = src->page_bytes;
   int peer = src->device == dst->device;
   if (!peer) TK_CUDA(cudaDeviceCanAccessPeer(&peer, src->device, dst->device));
-  if (peer) {
+  TK_CHECK(peer || engine != TK_SEND_SM, TK_EINVAL,
+           "tk_kv_send: TK_SEND_SM needs peer access from src to dst");
+  if (peer && engine != TK_SEND_CE) {
     // one copy kernel on the source GPU; a peer destination is written over NVLink
     int sms = 0;
     TK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, src->device));
@@ -990,7 +999,7 @@ int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
     if (rc) return rc;
   } else {
     for (int i = 0; i < n_pages;) {
-      // no peer path: copy engine, runs of consecutive pages coalesced
+      // copy engine (requested, or no peer path): runs of consecutive pages coalesced
       int j = i + 1;
       while (j < n_pages && src_pages[j] == src_pages[j - 1] + 1 &&
              dst_pages[j] == dst_pages[j - 1] + 1)
@@ -1374,6 +1383,42 @@ int tk_event_elapsed(tk_event* a, tk_event* b, int64_t* elapsed_ns) {
   float ms = 0.f;
   TK_CUDA(cudaEventElapsedTime(&ms, a->start, b->end));
   *elapsed_ns = static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+  return TK_OK;
+}
+
+int tk_device_memory(int32_t device, int64_t* free_bytes, int64_t* total_bytes) {
+  TK_CHECK(free_bytes && total_bytes, TK_EINVAL, "tk_device_memory: null argument");
+  int nd = 0;
+  TK_CUDA(cudaGetDeviceCount(&nd));
+  TK_CHECK(device >= 0 && device < nd, TK_EINVAL, "tk_device_memory: no such device");
+  TK_CUDA(cudaSetDevice(device));
+  size_t f = 0, t = 0;
+  TK_CUDA(cudaMemGetInfo(&f, &t));
+  *free_bytes = static_cast<int64_t>(f);
+  *total_bytes = static_cast<int64_t>(t);
+  return TK_OK;
+}
+
+int tk_event_anchor(int32_t device, tk_event** out) {
+  TK_CHECK(out, TK_EINVAL, "tk_event_anchor: null argument");
+  int nd = 0;
+  TK_CUDA(cudaGetDeviceCount(&nd));
+  TK_CHECK(device >= 0 && device < nd, TK_EINVAL, "tk_event_anchor: no such device");
+  TK_CUDA(cudaSetDevice(device));
+  std::unique_ptr<tk_event> ev(new tk_event());
+  ev->device = device;
+  TK_CUDA(cudaEventCreate(&ev->start));
+  TK_CUDA(cudaEventCreate(&ev->end));
+  // a marker on an otherwise idle stream; the caller reads its host clock
+  // right after this returns (completion -> return is a few microseconds)
+  cudaStream_t st;
+  TK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  TK_CUDA(cudaEventRecord(ev->start, st));
+  TK_CUDA(cudaEventRecord(ev->end, st));
+  TK_CUDA(cudaEventSynchronize(ev->end));
+  TK_CUDA(cudaStreamDestroy(st));
+  ev->finished = true;
+  *out = ev.release();
   return TK_OK;
 }
 

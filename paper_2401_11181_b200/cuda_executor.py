@@ -99,6 +99,9 @@ class _Then:
         self.ev.wait()
         return self.done()
 
+    def done_time(self):
+        return self.ev.done_time()
+
 
 class CudaExecutor:
     """Executor protocol of executor.py on real devices."""
@@ -121,6 +124,11 @@ class CudaExecutor:
         self.staging_pages = int(mcfg.get("staging_pages", 512))
         self.max_batch = int(mcfg.get("max_decode_batch", 256))
         self.device_predictor = bool(mcfg.get("device_predictor", True))
+        # handoff engine: "auto" (SM page-copy kernel, peer stores over NVLink),
+        # "sm", or "ce" (copy engines, leaves the SMs to the next chunk)
+        self.send_engine = str(mcfg.get("kv_send_engine", "auto"))
+        if self.send_engine not in native.SEND_ENGINES:
+            raise ValueError(f"model.kv_send_engine must be one of {sorted(native.SEND_ENGINES)}")
         self.insts: dict[str, native.Instance] = {}
         self.pools: dict[str, _Pool] = {}
         self.tables: dict[str, dict[int, list[int]]] = {}   # inst -> req -> pages
@@ -141,10 +149,49 @@ class CudaExecutor:
                       "decode_device_ns": 0, "handoff_device_ns": 0, "predict_calls": 0,
                       "flips": 0, "flip_host_us": 0.0}
         self._req_by_id: dict[int, Request] = {r.id: r for r in (requests or [])}
+        if mcfg.get("capacity_from_hbm"):
+            self._size_capacity_from_hbm(float(mcfg.get("hbm_reserve_gb", 6.0)))
+
+    def _size_capacity_from_hbm(self, reserve_gb: float) -> None:
+        """Decode KV capacity (``mem_capacity_tokens``, pdsim/costs.py:46) from the
+        free HBM of the decode GPUs: on each device
+        that holds a decode instance, free memory minus the weights (once per
+        device), the co-located prefill pools, each instance's receive staging
+        and scratch, and a reserve, divided among its decode instances.  The
+        smallest per-instance figure is every decode instance's capacity (the
+        cost model has one).  run_experiment builds the executor first and hands
+        the scheduler ``executor.params``."""
+        import dataclasses
+        cfg = self.config
+        ids = ([f"p{i}" for i in range(cfg.n_prefill)] + [f"d{i}" for i in range(cfg.n_decode)])
+        on: dict[int, list[str]] = {}
+        for iid in ids:
+            on.setdefault(self._device_of(iid), []).append(iid)
+        pb = self.shape.kv_bytes_per_token * self.page_tokens
+        weights = 2 * self.shape.params
+        best = None
+        for dev, here in on.items():
+            n_dec = sum(1 for i in here if i[0] == "d")
+            if not n_dec:
+                continue
+            free, _ = native.device_memory(dev)
+            avail = free - weights - reserve_gb * 1e9
+            avail -= sum(1 for i in here if i[0] == "p") * (self.prefill_pages * pb + 2e9)
+            per = avail / n_dec - self.staging_pages * pb - 2e9
+            pages = int(per // pb)
+            best = pages if best is None else min(best, pages)
+        if best is None:
+            return
+        if best < 64:
+            raise native.NativeError(f"capacity_from_hbm: only {best} KV pages fit on the decode GPUs")
+        tokens = best * self.page_tokens
+        self.params = dataclasses.replace(self.params, mem_capacity_tokens=tokens)
 
     # -- lifecycle ---------------------------------------------------------------------
     def _device_of(self, iid: str) -> int:
         return place_instance(iid, self.config.n_prefill, self.n_dev, self.devices)
+
+    device_of = _device_of
 
     def attach(self, inst) -> None:
         dev = self._device_of(inst.id)
@@ -270,7 +317,7 @@ class CudaExecutor:
             return _Then(ev, release_src_host)
         dst_pages = self.pools[dst].take(len(src_pages), dst)  # receive staging
         self.tables[dst][req.id] = dst_pages
-        ev = self.insts[src_id].kv_send(src_pages, self.insts[dst], dst_pages)
+        ev = self.insts[src_id].kv_send(src_pages, self.insts[dst], dst_pages, self.send_engine)
         self.stats["kv_bytes_sent"] += nbytes
 
         def release_src():
@@ -301,7 +348,8 @@ class CudaExecutor:
         if "host" in st:
             ev = self.insts[src_id].swap_out(src_pages[lo:hi], st["host"] + lo * pb)
         else:
-            ev = self.insts[src_id].kv_send(src_pages[lo:hi], self.insts[dst], st["dst"][lo:hi])
+            ev = self.insts[src_id].kv_send(src_pages[lo:hi], self.insts[dst], st["dst"][lo:hi],
+                                            self.send_engine)
         st["sent"] = max(lo, hi)
         nbytes = max(0, hi - lo) * pb
         self.stats["kv_bytes_sent"] += nbytes
@@ -467,6 +515,7 @@ class CudaExecutor:
         s = dict(self.stats)
         s["model"] = self.shape.name
         s["devices"] = {k: self._device_of(k) for k in self.insts}
+        s["mem_capacity_tokens"] = self.params.mem_capacity_tokens
         if s["prefill_device_ns"]:
             s["prefill_tok_s_device"] = s["prefill_tokens"] / (s["prefill_device_ns"] / 1e9)
         if s["decode_device_ns"]:

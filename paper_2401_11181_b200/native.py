@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import time
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -47,6 +48,7 @@ _SIGNATURES = {
     "tk_last_error": ([], C.c_char_p),
     "tk_version": ([], C.c_int),
     "tk_device_count": ([_I32P], C.c_int),
+    "tk_device_memory": ([C.c_int32, _I64P, _I64P], C.c_int),
     "tk_instance_create": ([C.c_int32, C.POINTER(tk_model_desc), C.c_uint64, C.c_int32, C.c_int32,
                             C.c_int32, C.POINTER(_P)], C.c_int),
     "tk_instance_destroy": ([_P], C.c_int),
@@ -60,6 +62,7 @@ _SIGNATURES = {
     "tk_decode_step": ([_P, C.c_int32, _I32P, _I32P, _I32P, C.c_int32, _I32P,
                         C.POINTER(C.c_float), C.POINTER(_P)], C.c_int),
     "tk_kv_send": ([_P, _I32P, _P, _I32P, C.c_int32, C.POINTER(_P)], C.c_int),
+    "tk_kv_send_ex": ([_P, _I32P, _P, _I32P, C.c_int32, C.c_int32, C.POINTER(_P)], C.c_int),
     "tk_predict": ([_P, _I32P, _I32P, C.c_int32, C.c_int32, _I32P, C.POINTER(_P)], C.c_int),
     "tk_predict_scores": ([_P, _I32P, _I32P, C.c_int32, C.c_int32, _I32P, C.POINTER(C.c_float),
                            C.POINTER(_P)], C.c_int),
@@ -72,6 +75,7 @@ _SIGNATURES = {
     "tk_event_release": ([_P], C.c_int),
     "tk_instance_sync": ([_P], C.c_int),
     "tk_event_elapsed": ([_P, _P, _I64P], C.c_int),
+    "tk_event_anchor": ([C.c_int32, C.POINTER(_P)], C.c_int),
     "tk_launch_count": ([_I64P], C.c_int),
     "tk_last_staged_bytes": ([_P, _I64P, _I64P], C.c_int),
     "tk_profile_enable": ([_P, C.c_int32], C.c_int),
@@ -100,6 +104,7 @@ _SIGNATURES = {
 }
 
 EXPORTED = tuple(_SIGNATURES)
+SEND_ENGINES = {"auto": 0, "sm": 1, "ce": 2}  # TK_SEND_* in include/tetri.h
 
 _lib: C.CDLL | None = None
 
@@ -205,11 +210,26 @@ MODELS = {m.name: m for m in (OPT_13B, OPT_125M, LLAMA2_7B, PREDICTOR_125M, TINY
 class Event:
     """A device completion handle (``done()`` for the engine, ``wait()``)."""
 
-    def __init__(self, ptr: C.c_void_p, keep=()):
+    def __init__(self, ptr: C.c_void_p, keep=(), device: int | None = None):
         self._ptr = ptr
         self._keep = keep  # host buffers that must outlive publication
         self._done = False
         self.elapsed_ns = 0
+        self.device = device
+        self._t_done: float | None = None
+
+    def done_time(self) -> float | None:
+        """Host ``time.perf_counter()`` of the device completion (the end marker
+        mapped through the device's anchor event), or None if not done."""
+        if not self._done or self.device is None:
+            return None
+        if self._t_done is None:
+            anchor, t0 = _anchor(self.device)
+            ns = C.c_int64()
+            check(load().tk_event_elapsed(anchor._ptr, self._ptr, C.byref(ns)),
+                  "tk_event_elapsed")
+            self._t_done = t0 + ns.value / 1e9
+        return self._t_done
 
     def done(self) -> bool:
         if self._done:
@@ -313,7 +333,7 @@ class Instance:
             self._h, n, ids, sl, len(slices), bt, len(block_tables), out,
             logits.ctypes.data_as(C.POINTER(C.c_float)) if want_logits and n_emit else None,
             C.byref(ev)), "tk_prefill_chunk")
-        e = Event(ev, keep=(ids, sl, bt, out))
+        e = Event(ev, keep=(ids, sl, bt, out), device=self.device)
         return (e, out, logits) if want_logits else (e, out)
 
     def decode_step(self, last_tokens, ctx_lens, block_tables, bt_stride, want_logits=False):
@@ -327,15 +347,23 @@ class Instance:
             self._h, b, ids, lens, bt, bt_stride, out,
             logits.ctypes.data_as(C.POINTER(C.c_float)) if want_logits else None,
             C.byref(ev)), "tk_decode_step")
-        e = Event(ev, keep=(ids, lens, bt, out))
+        e = Event(ev, keep=(ids, lens, bt, out), device=self.device)
         return (e, out, logits) if want_logits else (e, out)
 
-    def kv_send(self, src_pages, dst: "Instance", dst_pages) -> Event:
+    def kv_send(self, src_pages, dst: "Instance", dst_pages, engine: str = "auto") -> Event:
+        """engine: "auto" (tk_kv_send), "sm" (page-copy kernel; peer stores over
+        NVLink across devices) or "ce" (copy engines)."""
+        if engine not in SEND_ENGINES:
+            raise ValueError(f"engine must be one of {sorted(SEND_ENGINES)}")
         sp, dp = i32(src_pages), i32(dst_pages)
         ev = C.c_void_p()
-        check(load().tk_kv_send(self._h, sp, dst._h, dp, len(src_pages), C.byref(ev)),
-              "tk_kv_send")
-        return Event(ev, keep=(sp, dp))
+        if engine == "auto":
+            check(load().tk_kv_send(self._h, sp, dst._h, dp, len(src_pages), C.byref(ev)),
+                  "tk_kv_send")
+        else:
+            check(load().tk_kv_send_ex(self._h, sp, dst._h, dp, len(src_pages),
+                                       SEND_ENGINES[engine], C.byref(ev)), "tk_kv_send_ex")
+        return Event(ev, keep=(sp, dp), device=self.device)
 
     def predict(self, token_ids, lens, max_len: int = 512):
         out = (C.c_int32 * len(lens))()
@@ -343,7 +371,7 @@ class Instance:
         ev = C.c_void_p()
         check(load().tk_predict(self._h, ids, ls, len(lens), max_len, out, C.byref(ev)),
               "tk_predict")
-        return Event(ev, keep=(ids, ls, out)), out
+        return Event(ev, keep=(ids, ls, out), device=self.device), out
 
     def predict_scores(self, token_ids, lens, max_len: int = 512):
         """(buckets, fp32 scores [n, n_labels]) -- waits for the device."""
@@ -355,7 +383,7 @@ class Instance:
         check(load().tk_predict_scores(self._h, ids, ls, len(lens), max_len, out,
                                        scores.ctypes.data_as(C.POINTER(C.c_float)), C.byref(ev)),
               "tk_predict_scores")
-        e = Event(ev, keep=(ids, ls, out))
+        e = Event(ev, keep=(ids, ls, out), device=self.device)
         e.wait()
         return list(out), scores
 
@@ -363,13 +391,13 @@ class Instance:
         p = i32(pages)
         ev = C.c_void_p()
         check(load().tk_swap_out(self._h, p, len(pages), host_ptr, C.byref(ev)), "tk_swap_out")
-        return Event(ev, keep=(p,))
+        return Event(ev, keep=(p,), device=self.device)
 
     def swap_in(self, pages, host_ptr) -> Event:
         p = i32(pages)
         ev = C.c_void_p()
         check(load().tk_swap_in(self._h, p, len(pages), host_ptr, C.byref(ev)), "tk_swap_in")
-        return Event(ev, keep=(p,))
+        return Event(ev, keep=(p,), device=self.device)
 
     def sync(self) -> None:
         check(load().tk_instance_sync(self._h), "tk_instance_sync")
@@ -396,6 +424,21 @@ class Instance:
 
 
 PROFILE_KINDS = ("qkv_gemm", "o_gemm", "fc1_gemm", "fc2_gemm", "attention", "head_gemm", "other")
+
+
+_anchors: dict[int, tuple[Event, float]] = {}
+
+
+def _anchor(device: int) -> tuple[Event, float]:
+    """Per-device (anchor event, host perf_counter at its completion)."""
+    a = _anchors.get(device)
+    if a is None:
+        ev = C.c_void_p()
+        check(load().tk_event_anchor(device, C.byref(ev)), "tk_event_anchor")
+        t0 = time.perf_counter()
+        a = _anchors[device] = (Event(ev, device=device), t0)
+        a[0]._done = True
+    return a
 
 
 def event_elapsed_ns(first: Event, last: Event) -> int:
@@ -427,6 +470,13 @@ def device_count() -> int:
     n = C.c_int32()
     check(load().tk_device_count(C.byref(n)), "tk_device_count")
     return n.value
+
+
+def device_memory(device: int) -> tuple[int, int]:
+    """(free, total) HBM bytes of ``device``."""
+    f, t = C.c_int64(), C.c_int64()
+    check(load().tk_device_memory(device, C.byref(f), C.byref(t)), "tk_device_memory")
+    return f.value, t.value
 
 
 # ---------------------------------------------------------------- raw kernels (torch tensors)
