@@ -1000,18 +1000,20 @@ __global__ void __launch_bounds__(192, 1)
                          : p.exp == 2 ? 2 * A_BYTES
                          : p.exp == 3 ? PAIR_STAGE_BYTES - 2 * A_BYTES
                                       : PAIR_STAGE_BYTES;
-      auto load_a = [&](int ctile, int kb, int stage) {
+      // tile coordinates: A row of this CTA's 128-row m-tile, B row of its slice
+      auto a_row_of = [&](int ctile) { return ((ctile % groups_m) * CS + rank) * BM; };
+      auto b_row_of = [&](int ctile) {
+        return (ctile / groups_m) * BN + half * (BN / 2) + pair * SLICE_ROWS;
+      };
+      auto load_a_at = [&](int arow, int kb, int stage) {
         if (kGemmExp && p.exp == 3) return;
-        const int m_idx = (ctile % groups_m) * CS + rank;  // this CTA's 128-row tile
 #pragma unroll
         for (int s = 0; s < KS; ++s)
           tma_load_2d_pair(sa + stage * A_BYTES + s * A_BOX, &tmap_a, &full[stage],
-                           (kb * KS + s) * BK, m_idx * BM, pol_a);
+                           (kb * KS + s) * BK, arow, pol_a);
       };
-      auto load_b = [&](int ctile, int kb, int stage) {
+      auto load_b_at = [&](int brow, int kb, int stage) {
         if (kGemmExp && p.exp == 2) return;
-        const int n_idx = ctile / groups_m;
-        const int brow = n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS;
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
           uint8_t* bdst = sb + stage * BH_BYTES + s * BH_BOX + pair * SLICE_BYTES;
@@ -1022,6 +1024,8 @@ __global__ void __launch_bounds__(192, 1)
                                 pol_b);
         }
       };
+      auto load_a = [&](int ctile, int kb, int stage) { load_a_at(a_row_of(ctile), kb, stage); };
+      auto load_b = [&](int ctile, int kb, int stage) { load_b_at(b_row_of(ctile), kb, stage); };
       // optional L2 prefetch of this CTA's weight slice ahead of the ring (TK_GEMM_PF;
       // measured slower, off by default)
       const int pf_dist = p.pf_dist;
@@ -1056,15 +1060,22 @@ __global__ void __launch_bounds__(192, 1)
       }
       int stage = pre % STAGES;
       uint32_t phase = pre == STAGES ? 1u : 0u;
+      // steady state: the weight (B) slice first -- it comes from DRAM, A from L2
+      int arow = a_row_of(ctile), brow = b_row_of(ctile);
       for (long long i = it_begin + pre; i < it_end; ++i) {
         if (kGemmExp && pf_dist > 0) prefetch_b_upto(i + pf_dist + 1);
         gemm_stamp(p, 3, i - it_begin);
         mbar_wait(&empty[stage], phase ^ 1);
         gemm_stamp(p, 4, i - it_begin);
         if (leader) mbar_expect_tx(&full[stage], xbytes);
-        load_a(ctile, kb, stage);
-        load_b(ctile, kb, stage);
-        if (++kb == kbs) { kb = 0; ++ctile; }
+        load_b_at(brow, kb, stage);
+        load_a_at(arow, kb, stage);
+        if (++kb == kbs) {
+          kb = 0;
+          ++ctile;
+          arow = a_row_of(ctile);
+          brow = b_row_of(ctile);
+        }
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -1078,7 +1089,16 @@ __global__ void __launch_bounds__(192, 1)
     // counters stay in uniform registers); one elected lane issues tcgen05 ops.
     if (leader) {
       constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
-      const uint32_t sa_base = smem_u32(sa), sb_base = smem_u32(sb);
+      // Descriptors are built once; a stage's are the base plus a constant step
+      // (16-byte units of the start-address field, which cannot carry out of it:
+      // shared memory is < 256 KB), so the per-stage issue is a few uniform adds
+      // and the MMAs -- the issuing warp must stay ahead of the tensor pipe
+      // (72 cycles per 144-wide MMA).
+      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sa));
+      const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sb));
+      constexpr uint32_t A_STEP = A_BYTES >> 4, B_STEP = BH_BYTES >> 4;
+      const uint32_t empty0 = smem_u32(empty);
+      uint32_t a_off = 0, b_off = 0, bar_off = 0;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -1100,23 +1120,27 @@ __global__ void __launch_bounds__(192, 1)
           tc_fence_after();
           if (elect_one_sync()) {
             if (!kGemmExp || p.exp != 1) {
+              const uint64_t a_desc = a_desc0 + a_off, b_desc = b_desc0 + b_off;
+              umma_bf16_pair(d_tmem, a_desc, b_desc, idesc, k > 0 ? 1u : 0u);
 #pragma unroll
-              for (int s = 0; s < KS; ++s) {
-                const uint64_t a_desc = umma_desc_sw128(sa_base + stage * A_BYTES + s * A_BOX);
-                const uint64_t b_desc = umma_desc_sw128(sb_base + stage * BH_BYTES + s * BH_BOX);
-#pragma unroll
-                for (int kk = 0; kk < BK / 16; ++kk)  // +32 B per K step = +2 descriptor units
-                  umma_bf16_pair(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
-                                 (k > 0 || s > 0 || kk > 0) ? 1u : 0u);
+              for (int q = 1; q < KS * (BK / 16); ++q) {
+                // +32 B per K step = +2 descriptor units; KS boxes per stage
+                const uint32_t s = q / (BK / 16), kk = q % (BK / 16);
+                umma_bf16_pair(d_tmem, a_desc + s * (A_BOX >> 4) + 2 * kk,
+                               b_desc + s * (BH_BOX >> 4) + 2 * kk, idesc, 1u);
               }
             }
-            umma_commit_pair_mc(&empty[stage], all_mask);
+            umma_commit_pair_mc_addr(empty0 + bar_off, all_mask);
             gemm_stamp(p, 2, i - it_begin + k);
           }
           __syncwarp();
+          a_off += A_STEP;
+          b_off += B_STEP;
+          bar_off += 8;
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
+            a_off = b_off = bar_off = 0;
           }
         }
         if (elect_one_sync()) umma_commit_pair_mc(&tfull[acc], pair_mask);

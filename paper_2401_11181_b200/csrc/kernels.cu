@@ -11,6 +11,7 @@
 //   argmax             greedy token per row (first maximum, like torch.argmax)
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "tk_common.cuh"
 #include "tk_kernels.h"
@@ -253,7 +254,13 @@ int launch_add_norm(float* x, const __nv_bfloat16* delta, const __nv_bfloat16* w
            "norm: cols must be a multiple of 4 and <= 8192");
   if (rows == 0) return TK_OK;
   const __nv_bfloat16* bb = rms ? nullptr : b;
-  if (cols % 128 == 0 && cols <= 128 * 40) {
+  // The warp-per-row kernel measured slower in situ at 512 x 5120 (13.2 vs 11.6 us
+  // per launch, profiles/r02_experiments.md); kept as an experiment (TK_NORM_IMPL=warp).
+  static const int impl = [] {
+    const char* e = getenv("TK_NORM_IMPL");
+    return e && e[0] == 'w' ? 1 : 0;
+  }();
+  if (impl == 1 && cols % 128 == 0 && cols <= 128 * 40) {
     using WFn = void (*)(float*, const __nv_bfloat16*, const __nv_bfloat16*,
                          const __nv_bfloat16*, __nv_bfloat16*, int, int, float);
     WFn wk = nullptr;

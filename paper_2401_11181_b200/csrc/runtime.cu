@@ -611,6 +611,8 @@ int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed
                                                         std::min(inst->dec_max_ctx, 1 << 16));
   TK_CUDA(cudaMalloc(&inst->dec_ws, inst->dec_ws_bytes));
   TK_CUDA(cudaMalloc(&inst->attn_partial, attn_partial_bytes(m.n_heads, m.head_dim)));
+  // zeroed once: the attention kernel's per-group arrival counters live at its end
+  TK_CUDA(cudaMemset(inst->attn_partial, 0, attn_partial_bytes(m.n_heads, m.head_dim)));
   for (auto& s : inst->ring) {
     TK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.host), kSlotBytes, cudaHostAllocDefault));
     TK_CUDA(cudaMalloc(&s.dev, kSlotBytes));
@@ -1231,6 +1233,7 @@ static int chunk_attention_impl(const void* q, int32_t q_stride, void* o, const 
     if (cudaMalloc(&d, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
     dev.push_back(d);
     if (src && bytes && cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    if (!src && cudaMemset(d, 0, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
     return d;
   };
   struct Freer {

@@ -365,9 +365,12 @@ class CudaExecutor:
             self.host_staged.add(req.id)
             self.stats["kv_host_staged"] = self.stats.get("kv_host_staged", 0) + 1
 
+        parts = st["parts"]
+
         def release_src():
             self.pools[src_id].give(src_pages)
-            self.stats["handoff_device_ns"] += ev.elapsed_ns
+            # every part's copy time, not only the final part's
+            self.stats["handoff_device_ns"] += ev.elapsed_ns + sum(e.wait() for e in parts)
 
         return _Then(ev, release_src)
 

@@ -75,11 +75,13 @@ def test_kv_send_engines_bit_exact(engine, pair):
     p = native.Instance(model, device=src_dev, seed=5, kv_pages=n + 40, max_chunk=64)
     d = native.Instance(model, device=dst_dev, seed=5, kv_pages=n + 70, max_chunk=64)
     rng = np.random.default_rng(7)
-    src = rng.permutation(n + 40)[:n].tolist()
-    dst = rng.permutation(n + 70)[:n].tolist()
-    # runs of consecutive pages on both sides exercise the copy engine's coalescing
-    src[10:20] = list(range(n + 20, n + 30))
-    dst[10:20] = list(range(n + 50, n + 60))
+    # distinct pages, scattered, with one run of consecutive pages on both sides
+    # (the copy engine coalesces runs)
+    src_run, dst_run = list(range(n + 20, n + 30)), list(range(n + 50, n + 60))
+    src = [x for x in rng.permutation(n + 40).tolist() if x not in src_run][: n - 10]
+    dst = [x for x in rng.permutation(n + 70).tolist() if x not in dst_run][: n - 10]
+    src[10:10] = src_run
+    dst[10:10] = dst_run
     data = _seed_pages(p, src, rng)
     ev = p.kv_send(src, d, dst, engine)
     ev.wait()
@@ -129,7 +131,7 @@ def test_cross_gpu_handoff_then_decode_on_receiver():
 CFG = {
     "cluster": {"prefill": 1, "decode": 1},
     "workload": {"n_requests": 24, "mixture": {"LPLD": 0.5, "HPLD": 0.5},
-                 "lengths": {"heavy_prompt": {"hi": 1500}}},
+                 "lengths": {"heavy_prompt": {"hi": 900}}},
     "cost_model": {"preset": "nvlink300", "mem_capacity_tokens": 16000},
     "model": {"name": "tiny", "prefill_pages": 1024, "staging_pages": 256,
               "max_decode_batch": 64},
