@@ -448,6 +448,7 @@ def run_ours(args, world, rank, local):
         line["kv_handoff"] = guarded(lambda: handoff_run(args, shape, local, local, peaks))
         line["kv_handoff"]["overlap"] = guarded(lambda: overlap_run(args, shape, local, local))
         line["predictor"] = predictor_run(args, local, peaks)
+        line["predictor"]["corun"] = guarded(lambda: predictor_corun(args, shape, local))
     if n_gpus == 1 and not args.no_serving:
         line["serving"] = serving_run(args)
     if n_gpus == 1 and not args.no_cpu_baseline:
@@ -667,7 +668,7 @@ def predictor_run(args, device: int, peaks: dict, n: int = 16, length: int = 512
     for _ in range(3):
         inst.predict(ids, [length] * n, length)[0].wait()
     evs = [inst.predict(ids, [length] * n, length)[0] for _ in range(10)]
-    ns = native.event_elapsed_ns(evs[0], evs[-1]) / (len(evs) - 1)
+    ns = native.event_elapsed_ns(evs[0], evs[-1]) / len(evs)  # start of first .. end of last
     inst.close()
     params = 12 * (4 * 768 * 768 + 2 * 768 * 3072)
     flops = 2 * params * n * length + 4 * 768 * 12 * n * length * (length + 1) / 2
@@ -675,6 +676,64 @@ def predictor_run(args, device: int, peaks: dict, n: int = 16, length: int = 512
     return {"batch": n, "len": length, "device_us": round(ns / 1e3, 1),
             "tflops": round(tf, 1), "frac_of_peak": round(tf / peaks["bf16_tflops_sustained"], 4),
             "note": "tiny model: launch/latency bound, not tensor bound"}
+
+
+def predictor_corun(args, shape, device: int, prompt: int = 2048, reps: int = 5) -> dict:
+    """Parallel-mode predictor cost (pdsim/prefill.py:338-346; modeled as the 1.10
+    chunk tax, pdsim/costs.py:49; the paper measured +10% prefill latency,
+    PAPER.md:773-774): one round's prefill -- a ``prompt``-token request's 512-token
+    chunks on the OPT-13B prefill instance -- alone, and with the round's
+    predictor pass (16 x 512 tokens, OPT-125M-class) issued on its own instance's
+    stream just before the first chunk, as CudaExecutor.predict_round does."""
+    import random
+    import statistics as st
+
+    from paper_2401_11181_b200 import native
+    from paper_2401_11181_b200.workload import Request, token_ids_for
+    m = native.PREDICTOR_125M
+    pred = native.Instance(m, device=device, seed=args.seed + 1, kv_pages=16 * 32 + 8,
+                           max_chunk=16 * 512)
+    n_pages = (prompt + PAGE - 1) // PAGE
+    big = native.Instance(shape, device=device, seed=args.seed, kv_pages=n_pages,
+                          page_tokens=PAGE, max_chunk=CHUNK)
+    ids = token_ids_for(Request(id=0, arrival_us=0, prompt_len=prompt, true_decode_len=1),
+                        shape.vocab, args.seed)
+    bt = list(range(n_pages))
+    chunks = [(ids[c:c + CHUNK], [(c, CHUNK, 0, n_pages, int(c + CHUNK >= prompt))], bt)
+              for c in range(0, prompt, CHUNK)]
+    rng = random.Random(args.seed)
+    pids = [rng.randrange(2, m.vocab) for _ in range(16 * 512)]
+
+    def one(with_pred: bool, with_chunks: bool = True):
+        pev = pred.predict(pids, [512] * 16, 512)[0] if with_pred else None
+        evs = [big.prefill_chunk(*c)[0] for c in chunks] if with_chunks else []
+        if not evs:
+            return pev.wait(), 0, 0
+        chunk_ns = native.event_elapsed_ns(evs[0], evs[-1])
+        if pev is None:
+            return 0, chunk_ns, chunk_ns
+        span = max(native.event_elapsed_ns(pev, evs[-1]), native.event_elapsed_ns(pev, pev))
+        return native.event_elapsed_ns(pev, pev), chunk_ns, span
+
+    for _ in range(2):
+        one(True)
+    alone = st.median(one(False)[1] for _ in range(reps))
+    p_alone = st.median(one(True, False)[0] for _ in range(reps))
+    runs = [one(True) for _ in range(reps)]
+    p_under = st.median(r[0] for r in runs)
+    c_under = st.median(r[1] for r in runs)
+    span = st.median(r[2] for r in runs)
+    pred.close(), big.close()
+    return {"round": f"{prompt}-token prompt, {len(chunks)} chunks of 512 ({shape.name})",
+            "predictor": "16 x 512 tokens, OPT-125M-class classifier, own stream",
+            "round_alone_us": round(alone / 1e3, 1),
+            "predictor_alone_us": round(p_alone / 1e3, 1),
+            "round_with_predictor_us": round(c_under / 1e3, 1),
+            "predictor_under_round_us": round(p_under / 1e3, 1),
+            "makespan_us": round(span / 1e3, 1),
+            "measured_tax": round(span / alone, 4),
+            "reference_modeled_tax": 1.10,
+            "paper": "+10% prefill latency in parallel mode (PAPER.md:773-774)"}
 
 
 C3_MIX = {"LPLD": 0.5, "HPLD": 0.5}     # summarization-like (BASELINE configs[2])

@@ -149,6 +149,9 @@ class CudaExecutor:
                       "decode_device_ns": 0, "handoff_device_ns": 0, "predict_calls": 0,
                       "flips": 0, "flip_host_us": 0.0}
         self._req_by_id: dict[int, Request] = {r.id: r for r in (requests or [])}
+        # every generated token per request (first token, then one per decode step);
+        # kept when ``model.record_tokens`` is set (replay runs check them)
+        self.token_log: dict[int, list[int]] | None = {} if mcfg.get("record_tokens") else None
         if mcfg.get("capacity_from_hbm"):
             self._size_capacity_from_hbm(float(mcfg.get("hbm_reserve_gb", 6.0)))
 
@@ -286,11 +289,20 @@ class CudaExecutor:
 
         def publish():
             for idx, rid in emit_rids:
-                self.first_token[rid] = int(out[idx])
-                self.last_token[rid] = int(out[idx])
+                self._emit(rid, int(out[idx]), first=True)
             self.stats["prefill_device_ns"] += ev.elapsed_ns
 
         return _Then(ev, publish)
+
+    def _emit(self, rid: int, tok: int, first: bool = False) -> None:
+        if first:
+            self.first_token[rid] = tok
+        self.last_token[rid] = tok
+        if self.token_log is not None:
+            if first:
+                self.token_log[rid] = [tok]
+            else:
+                self.token_log[rid].append(tok)
 
     def round_done(self, inst, requests) -> None:
         pass
@@ -447,7 +459,7 @@ class CudaExecutor:
 
         def publish():
             for i, rid in enumerate(rids):
-                self.last_token[rid] = int(out[i])
+                self._emit(rid, int(out[i]))
             self.stats["decode_device_ns"] += ev.elapsed_ns
 
         return _Then(ev, publish), modeled
@@ -482,7 +494,7 @@ class CudaExecutor:
             ev, out = dev.decode_step(last, ctx, bt, stride)
             rids = [d.req.id for d in running]
             pending.append((ev, lambda out=out, rids=rids: [
-                self.last_token.__setitem__(r, int(out[i])) for i, r in enumerate(rids)]))
+                self._emit(r, int(out[i])) for i, r in enumerate(rids)]))
             self.stats["decode_steps"] += 1
             self.stats["decode_tokens"] += len(rids)
         by_id = {r.id: r for r in prefilling}
@@ -498,8 +510,7 @@ class CudaExecutor:
                     emit.append((len(slices) - 1, rid))
             ev, out = dev.prefill_chunk(ids, slices, bt)
             pending.append((ev, lambda out=out, emit=emit: [
-                (self.first_token.__setitem__(r, int(out[i])),
-                 self.last_token.__setitem__(r, int(out[i]))) for i, r in emit]))
+                self._emit(r, int(out[i]), first=True) for i, r in emit]))
             self.stats["prefill_tokens"] += len(ids)
             self.stats["prefill_chunks"] += 1
         if not pending:
@@ -526,3 +537,64 @@ class CudaExecutor:
         if s["handoff_device_ns"]:
             s["handoff_gb_s"] = s["kv_bytes_sent"] / s["handoff_device_ns"]
         return s
+
+
+class ReplayExecutor(CudaExecutor):
+    """Replay mode (SURVEY.md section 7 mode 2; ``executor: "replay"``): the
+    engine runs on pdsim's modeled clock, so every placement, chunk layout and
+    batch is the reference's own decision (the SimExecutor latencies,
+    pdsim/costs.py), while each decision is executed on the device -- every
+    chunk, handoff, swap and decode step -- synchronously, before its modeled
+    completion is scheduled.  The run therefore reproduces pdsim's decision trace
+    exactly *and* produces the tokens those decisions generate on the GPU
+    (``token_log``), which tests check against the fp32 oracle.  The device
+    model only executes: the cost model keeps the reference's constants
+    (kv_bytes_per_token, capacity), so any model shape can replay any config."""
+
+    def __init__(self, config, requests=None):
+        import dataclasses
+
+        from .executor import SimExecutor
+        mcfg = dict(config.model)
+        mcfg.pop("capacity_from_hbm", None)
+        mcfg.setdefault("record_tokens", True)
+        super().__init__(dataclasses.replace(config, model=mcfg), requests)
+        self.sim = SimExecutor(config.params)
+
+    @staticmethod
+    def _finish(handle) -> None:
+        wait = getattr(handle, "wait", None)
+        if wait is not None:
+            wait()
+        else:
+            handle.done()
+
+    def predict_round(self, inst, batch, predictor) -> int:
+        super().predict_round(inst, batch, predictor)
+        return self.sim.predict_round(inst, batch, predictor)
+
+    def prefill_chunk(self, inst, chunk, starting: int, tax: bool, extra) -> int:
+        self._finish(super().prefill_chunk(inst, chunk, starting, tax, extra))
+        return self.sim.prefill_chunk(inst, chunk, starting, tax, extra)
+
+    def kv_transfer(self, src_inst, req: Request, dst: str) -> int:
+        self._finish(super().kv_transfer(src_inst, req, dst))
+        return self.sim.kv_transfer(src_inst, req, dst)
+
+    def kv_stream(self, src_inst, req: Request, dst: str, start: int, end: int,
+                  final: bool) -> int:
+        self._finish(super().kv_stream(src_inst, req, dst, start, end, final))
+        return self.sim.kv_stream(src_inst, req, dst, start, end, final)
+
+    def decode_step(self, inst, running, kv_tokens: int, swapped_out: int,
+                    swapped_in: int) -> tuple[int, int]:
+        handle, modeled = super().decode_step(inst, running, kv_tokens, swapped_out, swapped_in)
+        self._finish(handle)
+        return modeled, modeled
+
+    def mixed_step(self, inst, prefilling, running, prefill_tokens, kv_tokens, swapped_out,
+                   swapped_in) -> tuple[int, int]:
+        handle, modeled = super().mixed_step(inst, prefilling, running, prefill_tokens,
+                                             kv_tokens, swapped_out, swapped_in)
+        self._finish(handle)
+        return modeled, modeled

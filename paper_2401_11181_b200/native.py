@@ -201,8 +201,12 @@ PREDICTOR_125M = ModelShape("opt-125m-cls", TK_ARCH_OPT, 12, 768, 12, 3072, 5027
 # Small shapes for parity tests (fast on the fp32 CPU oracle).
 TINY_OPT = ModelShape("tiny", TK_ARCH_OPT, 2, 256, 2, 1024, 1024, max_positions=1024)
 TINY_LLAMA = ModelShape("tiny-llama", TK_ARCH_LLAMA, 2, 256, 2, 768, 1024, max_positions=1024)
+# Tiny OPT whose position table covers pdsim's longest request (8192-token prompt +
+# 2048 decodes): replays of the reference's default workloads (executor "replay").
+TINY_LONG = ModelShape("tiny-long", TK_ARCH_OPT, 2, 256, 2, 1024, 1024, max_positions=10240)
 
-MODELS = {m.name: m for m in (OPT_13B, OPT_125M, LLAMA2_7B, PREDICTOR_125M, TINY_OPT, TINY_LLAMA)}
+MODELS = {m.name: m for m in (OPT_13B, OPT_125M, LLAMA2_7B, PREDICTOR_125M, TINY_OPT, TINY_LLAMA,
+                              TINY_LONG)}
 
 
 # ---------------------------------------------------------------- handles

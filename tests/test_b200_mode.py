@@ -37,6 +37,16 @@ def test_cuda_mode_rejects_a_kv_bytes_mismatch():
         tk.config_from_dict({"executor": "cuda", "model": {"name": "gpt-5"}})
 
 
+def test_replay_mode_keeps_the_reference_cost_model():
+    """executor "replay" (decisions on pdsim's modeled clock, executed on the
+    device): the cost model keeps the reference constants whatever model runs."""
+    cfg = tk.config_from_dict({"executor": "replay", "model": {"name": "tiny-long"}})
+    assert cfg.params.kv_bytes_per_token == 819_200
+    assert cfg.params == tk.config_from_dict({}).params
+    with pytest.raises(ConfigError, match="executor"):
+        tk.config_from_dict({"executor": "emulate"})
+
+
 class _Work:
     """A device handle: completes at host time ``t`` (perf_counter seconds)."""
 
