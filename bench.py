@@ -736,6 +736,76 @@ def predictor_corun(args, shape, device: int, prompt: int = 2048, reps: int = 5)
             "paper": "+10% prefill latency in parallel mode (PAPER.md:773-774)"}
 
 
+def c1_cpu_sample(args, seconds: float = 12.0) -> dict:
+    """BASELINE.json configs[0] / BASELINE.md section 4 item 2: the fp32 oracle runs
+    the tiny decoder (OPT-125M shape, all 12 layers, LM head) on the host cores over
+    a bounded sample of the same Mixed-128 workload: the first SJF round's chunks
+    (ChunkSize 512, pdsim/prefill.py:140-165) for ~``seconds``/2, then decode steps
+    of the prefilled requests as one batch for the rest."""
+    import torch
+
+    import paper_2401_11181_b200 as tk
+    from oracle.model_ref import ARCH_OPT, OracleModel, PagedCache, Shape, random_weights
+    from paper_2401_11181_b200 import native, workload
+    from paper_2401_11181_b200.engine import RngStreams
+    from paper_2401_11181_b200.prefill import chunkify
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    m = native.OPT_125M
+    shape = Shape(ARCH_OPT, m.n_layers, m.hidden, m.n_heads, m.ffn, m.vocab, m.max_positions)
+    ora = OracleModel(shape, random_weights(shape, args.seed))
+    cfg = tk.config_from_dict({"workload": {"n_requests": 128}})
+    reqs = workload.generate(cfg.workload_spec, RngStreams(args.seed).stream("workload"))
+    batch = sorted(reqs[:16], key=lambda r: (r.prompt_len, r.arrival_us, r.id))
+    tables, nxt = {}, 0
+    for r in batch:
+        k = (r.prompt_len + 64 + PAGE - 1) // PAGE
+        tables[r.id] = list(range(nxt, nxt + k))
+        nxt += k
+    cache = PagedCache(shape, nxt, PAGE)
+    prompts = {r.id: workload.token_ids_for(r, m.vocab, args.seed) for r in batch}
+    lens = {r.id: r.prompt_len for r in batch}
+    p_tok, p_s, done = 0, 0.0, set()
+    for c in chunkify(batch, 512):
+        ids, slices, bt = [], [], []
+        for rid, st, n in c.slices:
+            ids += prompts[rid][st:st + n]
+            slices.append((st, n, len(bt), len(tables[rid]), int(st + n == lens[rid])))
+            bt += tables[rid]
+            if st + n == lens[rid]:
+                done.add(rid)
+        t = time.perf_counter()
+        ora.prefill_chunk(cache, ids, slices, bt)
+        p_s += time.perf_counter() - t
+        p_tok += len(ids)
+        if p_s > seconds / 2:
+            break
+    rids = [r.id for r in batch if r.id in done]
+    d_tok, d_s, step = 0, 0.0, 0
+    while rids and d_s < seconds / 2 and step < 64:
+        t = time.perf_counter()
+        ora.decode_step(cache, [7] * len(rids), [lens[r] + step for r in rids],
+                        [tables[r] for r in rids])
+        d_s += time.perf_counter() - t
+        d_tok += len(rids)
+        step += 1
+    return {"prefill_tok_s": round(p_tok / p_s, 1) if p_s else None,
+            "decode_tok_s": round(d_tok / d_s, 1) if d_s else None, "cores": cores,
+            "kind": "port",
+            "sample": f"fp32 oracle, OPT-125M shape (12 layers + LM head): {p_tok} prompt tokens "
+                      f"of the first SJF round's chunks, then {step} decode steps of a batch of "
+                      f"{len(rids)} prefilled requests (Mixed-128 seed {args.seed})"}
+
+
+def c1_run(args) -> dict:
+    """BASELINE.json configs[0] on the device: the tiny decoder (OPT-125M shape),
+    ChunkSize 512, 1 prefill + 1 decode instance (co-located on one GPU), the
+    four-class Mixed-128 workload; beside it the fp32 oracle on the host cores."""
+    return {"device": guarded(lambda: serving_leg(args, 1, 1, 128, model="opt-125m",
+                                                  colocate=True)),
+            "cpu_oracle": guarded(lambda: c1_cpu_sample(args))}
+
+
 C3_MIX = {"LPLD": 0.5, "HPLD": 0.5}     # summarization-like (BASELINE configs[2])
 C5_MIX = {"LPHD": 0.5, "HPHD": 0.5}     # content creation (BASELINE configs[4])
 
@@ -838,6 +908,7 @@ def serving_run(args) -> dict:
                                                            coupled=True))
     out["c5proxy_llama_lphd_hphd_1p1d"] = guarded(
         lambda: serving_leg(args, 1, 1, n, mixture=C5_MIX, model="llama-2-7b", colocate=True))
+    out["c1_tiny_decoder_1p1d"] = c1_run(args)
     return out
 
 

@@ -192,7 +192,9 @@ class ModelShape:
 # OPT-13B shape with the learned-position table extended to cover 8k prompts
 # plus 2k decodes (random weights; SURVEY.md §7 "hard parts").
 OPT_13B = ModelShape("opt-13b", TK_ARCH_OPT, 40, 5120, 40, 20480, 50272, max_positions=10240)
-OPT_125M = ModelShape("opt-125m", TK_ARCH_OPT, 12, 768, 12, 3072, 50272, max_positions=2048)
+# OPT-125M ("the tiny decoder", BASELINE.json configs[0]) with the position table
+# extended like OPT-13B's so the four-class workload's 8k+2k requests fit.
+OPT_125M = ModelShape("opt-125m", TK_ARCH_OPT, 12, 768, 12, 3072, 50272, max_positions=10240)
 LLAMA2_7B = ModelShape("llama-2-7b", TK_ARCH_LLAMA, 32, 4096, 32, 11008, 32000,
                        max_positions=4096, norm_eps=1e-5)
 # OPT-125M-shaped predictor with the 41-bucket score head (g=200, 8192 max).
