@@ -907,7 +907,13 @@ __global__ void __launch_bounds__(192, 1)
   constexpr int BM = 128, BK = 64;
   // BN % 32 != 0 (144): data-parallel one-tile-per-CTA schedules with a staged bf16
   // epilogue only (the host guarantees it); the last 32-column chunk is half used
-  static_assert(BN % 16 == 0 && BN <= 256 && (BN / 2 / (CS / 2)) % 8 == 0, "pair tile width");
+  // CS = 2: one pair; CS = 4: two pairs along M (all 512 rows) sharing every B half;
+  // CS = 8: 2 x 2 pairs -- two along M share B halves, two along N share A tiles, so
+  // every A and B byte of the cluster's 512 x 2BN block is fetched from L2 once.
+  constexpr int NMP = CS == 8 ? 2 : CS / 2;  // pairs along M (share each B half)
+  constexpr int NNP = CS == 8 ? 2 : 1;       // pairs along N (share each A tile)
+  constexpr int MT = 2 * NMP;                // 128-row m-tiles per cluster
+  static_assert(BN % 16 == 0 && BN <= 256 && (BN / 2 / NMP) % 8 == 0, "pair tile width");
   constexpr int NCH = (BN + 31) / 32;
   constexpr int STAGES = PairCfg<BN, KS>::STAGES;
   constexpr int A_BOX = BM * BK * 2;          // own 128 rows of one 64-wide k-block
@@ -917,8 +923,10 @@ __global__ void __launch_bounds__(192, 1)
   constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
   constexpr int PAIR_STAGE_BYTES = 2 * STAGE_BYTES;
   constexpr int NPAIRS = CS / 2;
-  constexpr int SLICE_ROWS = (BN / 2) / NPAIRS;  // B-half rows each CTA loads
+  constexpr int SLICE_ROWS = (BN / 2) / NMP;        // B-half rows each CTA loads
   constexpr int SLICE_BYTES = SLICE_ROWS * BK * 2;  // per k-block box
+  constexpr int A_SLICE_ROWS = BM / NNP;            // A rows each CTA loads
+  constexpr int A_SLICE_BYTES = A_SLICE_ROWS * BK * 2;
   constexpr int TMEM_COLS = 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -939,18 +947,20 @@ __global__ void __launch_bounds__(192, 1)
   const int pair = rank >> 1;
   const int half = rank & 1;
   const bool leader = half == 0;
+  const int mp = pair % NMP, np = pair / NMP;  // position of the pair in the cluster
+  const int m_local = mp * 2 + half;           // this CTA's 128-row m-tile in the cluster
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
     if (p.entry_pf) {
       // The first ring fill's weight tiles come from DRAM: start pulling them into L2
       // now, while the barriers, TMEM and the cluster are being set up.
-      const int cl = blockIdx.x / CS, g = gridDim.x / CS, gm = p.tiles_m / CS;
+      const int cl = blockIdx.x / CS, g = gridDim.x / CS, gm = p.tiles_m / MT;
       const long long b0 = static_cast<long long>(cl) * p.total_iters / g;
       const long long b1 = static_cast<long long>(cl + 1) * p.total_iters / g;
       int ct = static_cast<int>(b0 / p.kbs), kq = static_cast<int>(b0 % p.kbs);
       for (long long i = b0; i < b1 && i < b0 + STAGES; ++i) {
-        const int row = (ct / gm) * BN + half * (BN / 2) + pair * ((BN / 2) / (CS / 2));
+        const int row = (ct / gm) * NNP * BN + np * BN + half * (BN / 2) + mp * SLICE_ROWS;
 #pragma unroll
         for (int s = 0; s < KS; ++s) tma_prefetch_2d(&tmap_b, (kq * KS + s) * BK, row);
         if (++kq == p.kbs) { kq = 0; ++ct; }
@@ -975,16 +985,20 @@ __global__ void __launch_bounds__(192, 1)
 
   const int cluster = blockIdx.x / CS;
   const int G = gridDim.x / CS;
-  const int groups_m = p.tiles_m / CS;  // 128-row m-tiles per cluster m-group = CS
+  const int groups_m = p.tiles_m / MT;  // cluster m-groups of MT 128-row m-tiles
   const long long T = p.total_iters;
   const long long it_begin = static_cast<long long>(cluster) * T / G;
   const long long it_end = static_cast<long long>(cluster + 1) * T / G;
   const int kbs = p.kbs;
   const uint16_t all_mask = static_cast<uint16_t>((1u << CS) - 1);
   const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * pair));
-  // CTAs holding this CTA's B half in any pair: ranks {half, half+2, ...}
-  const uint16_t half_mask = static_cast<uint16_t>(CS == 4 ? ((1u << half) | (1u << (half + 2)))
-                                                           : (1u << half));
+  // CTAs holding this CTA's B half (same n-pair and half, every m-pair), and its A
+  // tile (same m-pair and half, every n-pair)
+  uint16_t half_mask = 0, a_mask = 0;
+#pragma unroll
+  for (int q = 0; q < NMP; ++q) half_mask |= static_cast<uint16_t>(1u << ((np * NMP + q) * 2 + half));
+#pragma unroll
+  for (int q = 0; q < NNP; ++q) a_mask |= static_cast<uint16_t>(1u << ((q * NMP + mp) * 2 + half));
 
   // programmatic dependent launch: everything but the producer's first weight
   // tiles waits for the previous kernel on the stream
@@ -1001,23 +1015,30 @@ __global__ void __launch_bounds__(192, 1)
                          : p.exp == 3 ? PAIR_STAGE_BYTES - 2 * A_BYTES
                                       : PAIR_STAGE_BYTES;
       // tile coordinates: A row of this CTA's 128-row m-tile, B row of its slice
-      auto a_row_of = [&](int ctile) { return ((ctile % groups_m) * CS + rank) * BM; };
+      auto a_row_of = [&](int ctile) {
+        return ((ctile % groups_m) * MT + m_local) * BM + np * A_SLICE_ROWS;
+      };
       auto b_row_of = [&](int ctile) {
-        return (ctile / groups_m) * BN + half * (BN / 2) + pair * SLICE_ROWS;
+        return (ctile / groups_m) * NNP * BN + np * BN + half * (BN / 2) + mp * SLICE_ROWS;
       };
       auto load_a_at = [&](int arow, int kb, int stage) {
         if (kGemmExp && p.exp == 3) return;
 #pragma unroll
-        for (int s = 0; s < KS; ++s)
-          tma_load_2d_pair(sa + stage * A_BYTES + s * A_BOX, &tmap_a, &full[stage],
-                           (kb * KS + s) * BK, arow, pol_a);
+        for (int s = 0; s < KS; ++s) {
+          if constexpr (NNP == 1)
+            tma_load_2d_pair(sa + stage * A_BYTES + s * A_BOX, &tmap_a, &full[stage],
+                             (kb * KS + s) * BK, arow, pol_a);
+          else
+            tma_load_2d_pair_mc(sa + stage * A_BYTES + s * A_BOX + np * A_SLICE_BYTES, &tmap_a,
+                                &full[stage], (kb * KS + s) * BK, arow, a_mask, pol_a);
+        }
       };
       auto load_b_at = [&](int brow, int kb, int stage) {
         if (kGemmExp && p.exp == 2) return;
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
-          uint8_t* bdst = sb + stage * BH_BYTES + s * BH_BOX + pair * SLICE_BYTES;
-          if constexpr (CS == 2)
+          uint8_t* bdst = sb + stage * BH_BYTES + s * BH_BOX + mp * SLICE_BYTES;
+          if constexpr (NMP == 1)
             tma_load_2d_pair(bdst, &tmap_b, &full[stage], (kb * KS + s) * BK, brow, pol_b);
           else
             tma_load_2d_pair_mc(bdst, &tmap_b, &full[stage], (kb * KS + s) * BK, brow, half_mask,
@@ -1034,7 +1055,7 @@ __global__ void __launch_bounds__(192, 1)
       auto prefetch_b_upto = [&](long long upto) {
         for (; pf_i < upto && pf_i < it_end; ++pf_i) {
           const int n_idx = pf_tile / groups_m;
-          tma_prefetch_2d(&tmap_b, pf_kb * KS * BK, n_idx * BN + half * (BN / 2) + pair * SLICE_ROWS);
+          tma_prefetch_2d(&tmap_b, pf_kb * KS * BK, n_idx * NNP * BN + np * BN + half * (BN / 2) + mp * SLICE_ROWS);
           if (++pf_kb == kbs) { pf_kb = 0; ++pf_tile; }
         }
       };
@@ -1162,8 +1183,8 @@ __global__ void __launch_bounds__(192, 1)
       const int ctile = static_cast<int>(i / kbs);
       const long long tile_first = static_cast<long long>(ctile) * kbs;
       const long long seg_end = min(it_end, tile_first + kbs);
-      const int m_idx = (ctile % groups_m) * CS + rank;
-      const int n_idx = ctile / groups_m;
+      const int m_idx = (ctile % groups_m) * MT + m_local;
+      const int n_idx = (ctile / groups_m) * NNP + np;
       const int tile = n_idx * p.tiles_m + m_idx;
       const int row = m_idx * BM + row_in_tile;
       const int col_base = n_idx * BN;
@@ -1407,6 +1428,7 @@ struct GemmEnv {
   int entry_pf = -1;                // TK_GEMM_ENTRY_PF
   int skinny_ctas = 0;              // TK_GEMM_SKINNY_CTAS: CTA cap of the decode GEMMs
   bool no144 = false;               // TK_NO_144: keep 160-wide 4-CTA clusters
+  bool cs8 = false;                 // TK_GEMM_CS8=1: 8-CTA (2 x 2 pair) clusters, experiments
   int pf_partials = -1;             // TK_GEMM_PFPART
   GemmEnv() {
     no_skinny = getenv("TK_NO_SKINNY") != nullptr;
@@ -1424,6 +1446,7 @@ struct GemmEnv {
     if (const char* f = getenv("TK_GEMM_ENTRY_PF")) entry_pf = atoi(f);
     if (const char* f = getenv("TK_GEMM_SKINNY_CTAS")) skinny_ctas = atoi(f);
     no144 = getenv("TK_NO_144") != nullptr;
+    if (const char* f = getenv("TK_GEMM_CS8")) cs8 = atoi(f) != 0;
     if (const char* f = getenv("TK_GEMM_PFPART")) pf_partials = atoi(f);
     if (const char* c = getenv("TK_GEMM_MAX_CTAS")) max_ctas = atoi(c);
   }
@@ -1628,6 +1651,18 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
     }
   }
   pl.tiles_n = (N + pl.bn - 1) / pl.bn;
+  // 8-CTA clusters (2 x 2 pairs: A shared along N as well as B along M) for the
+  // 256-wide stream-K schedule: a third less L2->SM traffic per FLOP, but only 12
+  // such clusters (96 SMs) are co-resident on a B200, so it is off by default
+  // (TK_GEMM_CS8=1; profiles/r02_experiments.md)
+  if (pl.pair && pl.bn == 256 && pl.cs == 4 && !data_parallel && pl.tiles_n % 2 == 0 &&
+      genv().cs8 && genv().fcs == 0) {
+    const int c8 = max_pair_clusters(8);
+    if (c8 >= 8) {
+      pl.cs = 8;
+      clusters = max_ctas > 0 ? std::min(c8, std::max(1, max_ctas / 8)) : c8;
+    }
+  }
   pl.ks = 1;
   // 160-wide tiles: two k-blocks per ring stage (O-proj at M=512: 34.8 -> 32.8 us,
   // the per-launch fill cost halves); TK_GEMM_KS=1 restores one
@@ -1636,7 +1671,10 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
     pl.ks = 2;
     pl.kbs /= 2;
   }
-  pl.total_iters = static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
+  // cluster tiles: (tiles_m / MT) m-groups x (tiles_n / NNP) n-groups
+  pl.total_iters = pl.cs == 8
+                       ? static_cast<long long>(pl.tiles_m / 4) * (pl.tiles_n / 2) * pl.kbs
+                       : static_cast<long long>(pl.tiles_m / pl.cs) * pl.tiles_n * pl.kbs;
   clusters = static_cast<int>(std::min<long long>(clusters, std::max<long long>(1, pl.total_iters / 4)));
   // Long K (FC2: 320 k-blocks per tile) amortises a split tile's exchange: use
   // every cluster; short K prefers the count with the fewest split tiles.
@@ -1780,7 +1818,11 @@ static int query_pair_clusters() {
 }
 
 static int max_pair_clusters(int cs) {
-  static int c2 = 0, c4 = 0;
+  static int c2 = 0, c4 = 0, c8 = 0;
+  if (cs == 8) {
+    if (!c8) c8 = query_pair_clusters<8>();
+    return c8;
+  }
   if (cs == 4) {
     if (!c4) c4 = query_pair_clusters<4>();
     return c4;
@@ -2005,8 +2047,14 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
       if (rc) return rc;
       return pair_epi<2, 144>(ta, tb, a, pl144.clusters, stream, pl144.ks);
     }
-    rc = make_tmap_kmajor(&tb, B, N, K, pl.bn / 2 / (pl.cs / 2));
+    rc = make_tmap_kmajor(&tb, B, N, K, pl.bn / 2 / (pl.cs == 8 ? 2 : pl.cs / 2));
     if (rc) return rc;
+    if (pl.cs == 8) {
+      // each CTA loads half of its A tile (64 rows) and multicasts it to its N-neighbour
+      rc = make_tmap_kmajor(&ta, A, M, K, 64);
+      if (rc) return rc;
+      return pair_epi<8, 256>(ta, tb, a, pl.clusters, stream, pl.ks);
+    }
     if (pl.bn == 160) {
       if (pl.cs == 4) return pair_epi<4, 160>(ta, tb, a, pl.clusters, stream, pl.ks);
       return pair_epi<2, 160>(ta, tb, a, pl.clusters, stream, pl.ks);

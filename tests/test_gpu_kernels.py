@@ -45,7 +45,9 @@ def _rel_err(x, ref):
     (907, 768, 768),     # BN=128 with a 4-CTA cluster (predictor O-proj)
     (907, 768, 3072),    # same, FC2
     (512, 5120, 20480),  # FC2: stream-K, final fixups through the bulk-copied partials
-    (512, 20480, 5120),  # FC1: split tiles mid-range and at the end
+    (512, 20480, 5120),  # FC1: split tiles mid-range and at the end (8-CTA clusters)
+    (512, 15360, 5120),  # QKV shape: 2 x 2 pairs per cluster, A and B multicast
+    (1024, 5120, 5120),  # two cluster m-groups of the 8-CTA schedule
     (512, 2560, 20480),  # 3-4 contributors per tile (partials beyond the ring: register path)
 ])
 def test_gemm_matches_fp32(M, N, K):
