@@ -796,8 +796,10 @@ int launch_attn_combine(__nv_bfloat16* o, const AttnQBlock* qblocks, int n_qbloc
 constexpr int kDecSplitTokens = 256;
 
 // grid (splits, heads, batch), 128 threads; each warp walks pages of the split.
-// Lane l owns dims [(l%16)*8, +8) of token parity l/16 inside each 16-token load
-// group; partial (m, l, acc) of the 4 warps are merged in smem.
+// A token's D dims are spread over D/8 lanes (16-byte loads), so one warp load
+// covers 32/(D/8) tokens (2 at D=128, 4 at D=64 -- the OPT-125M tiny decoder): lane l
+// owns dims [(l % LPT)*8, +8) of token group l / LPT; partial (m, l, acc) of the 4
+// warps are merged in smem.
 template <int D>
 __global__ void __launch_bounds__(128)
     decode_attn_kernel(const __nv_bfloat16* __restrict__ q, int q_stride,
@@ -807,13 +809,16 @@ __global__ void __launch_bounds__(128)
                        const int32_t* __restrict__ ctx_lens, float scale_log2,
                        float* __restrict__ ws, int max_splits, int split_tokens) {
   griddep_wait();  // q / pages from the QKV GEMM + kv_write (PDL launch)
-  static_assert(D == 128, "decode attention: head_dim 128");
+  static_assert(D == 128 || D == 64, "decode attention: head_dim 128 or 64");
+  constexpr int LPT = D / 8;      // lanes per token
+  constexpr int TPL = 32 / LPT;   // tokens per warp load
+  constexpr int ITER = 16 / TPL;  // loads per 16-token page
   const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
   const int ctx = ctx_lens[b];
   const int n_splits = (ctx + split_tokens - 1) / split_tokens;
   if (split >= n_splits) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = lane >> 4, dl = (lane & 15) * 8;
+  const int half = lane / LPT, dl = (lane % LPT) * 8;  // half: token group of the lane
   const int pt = g.page_tokens;  // 16
   const int t0 = split * split_tokens;
   const int t1 = min(ctx, t0 + split_tokens);
@@ -835,39 +840,38 @@ __global__ void __launch_bounds__(128)
     const int page = pages[base / pt];
     const __nv_bfloat16* kp = pool + g.offset(page, layer, 0, head, 0);
     const __nv_bfloat16* vp = pool + g.offset(page, layer, 1, head, 0);
-    uint4 kr[8], vr[8];
+    uint4 kr[ITER], vr[ITER];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int tok = 2 * i + half;
+    for (int i = 0; i < ITER; ++i) {
+      const int tok = TPL * i + half;
       kr[i] = __ldg(reinterpret_cast<const uint4*>(kp + tok * D + dl));
       vr[i] = __ldg(reinterpret_cast<const uint4*>(vp + tok * D + dl));
     }
-    float sc[8];
+    float sc[ITER];
     float pmax = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < ITER; ++i) {
       const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(&kr[i]);
       float d = 0.f;
 #pragma unroll
       for (int e = 0; e < 8; ++e) d += qv[e] * __bfloat162float(kb[e]);
-      d += __shfl_xor_sync(0xffffffffu, d, 8);
-      d += __shfl_xor_sync(0xffffffffu, d, 4);
-      d += __shfl_xor_sync(0xffffffffu, d, 2);
-      d += __shfl_xor_sync(0xffffffffu, d, 1);
-      const int tok = base + 2 * i + half;
+#pragma unroll
+      for (int off = LPT / 2; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+      const int tok = base + TPL * i + half;
       sc[i] = tok < t1 ? d : -INFINITY;
       pmax = fmaxf(pmax, sc[i]);
     }
-    pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 16));
+#pragma unroll
+    for (int off = LPT; off < 32; off <<= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, off));
     const float mn = fmaxf(m, pmax);
     const float corr = exp2f(m - mn);
     l *= corr;
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] *= corr;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < ITER; ++i) {
       // slots past the context may hold stale bytes (even NaN patterns): skip them
-      if (base + 2 * i + half < t1) {
+      if (base + TPL * i + half < t1) {
         const float p = exp2f(sc[i] - mn);
         l += p;
         const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&vr[i]);
@@ -877,10 +881,13 @@ __global__ void __launch_bounds__(128)
     }
     m = mn;
   }
-  // merge the two token-parity halves of the warp (same m)
-  l += __shfl_xor_sync(0xffffffffu, l, 16);
+  // merge the token groups of the warp (same m)
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+  for (int off = LPT; off < 32; off <<= 1) {
+    l += __shfl_xor_sync(0xffffffffu, l, off);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], off);
+  }
 
   // merge 4 warps
   __shared__ float s_m[4], s_l[4];
@@ -953,7 +960,8 @@ int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16*
                             KvGeom g, int layer, const int32_t* block_tables, int bt_stride,
                             const int32_t* ctx_lens, int batch, int max_ctx, float scale,
                             void* workspace, int64_t ws_bytes, cudaStream_t s) {
-  TK_CHECK(g.head_dim == 128, TK_EUNSUPPORTED, "decode attention: head_dim must be 128");
+  TK_CHECK(g.head_dim == 128 || g.head_dim == 64, TK_EUNSUPPORTED,
+           "decode attention: head_dim must be 128 or 64");
   TK_CHECK(g.page_tokens == 16, TK_EUNSUPPORTED, "decode attention: page_tokens must be 16");
   TK_CHECK(ws_bytes >= decode_attention_workspace_bytes(batch, g.n_heads, g.head_dim, max_ctx),
            TK_EINVAL, "decode attention: workspace too small");
@@ -969,14 +977,16 @@ int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16*
   const int splits = (max_ctx + split_tokens - 1) / split_tokens;
   const int ws_splits = (max_ctx + kDecSplitTokens - 1) / kDecSplitTokens;  // workspace stride
   const float scale_log2 = scale * 1.4426950408889634f;
-  TK_CUDA(launch_pdl(decode_attn_kernel<128>, dim3(splits, g.n_heads, batch), dim3(128), 0, s, q,
-                     q_stride, o, pool, g, layer, block_tables, bt_stride, ctx_lens, scale_log2,
+  const bool d64 = g.head_dim == 64;
+  TK_CUDA(launch_pdl(d64 ? decode_attn_kernel<64> : decode_attn_kernel<128>,
+                     dim3(splits, g.n_heads, batch), dim3(128), 0, s, q, q_stride, o, pool, g,
+                     layer, block_tables, bt_stride, ctx_lens, scale_log2,
                      static_cast<float*>(workspace), ws_splits, split_tokens));
   note_launch();
   if (splits > 1) {
-    TK_CUDA(launch_pdl(decode_combine_kernel<128>, dim3(g.n_heads, batch), dim3(128), 0, s, o,
-                       g.n_heads, ctx_lens, static_cast<const float*>(workspace), ws_splits,
-                       split_tokens));
+    TK_CUDA(launch_pdl(d64 ? decode_combine_kernel<64> : decode_combine_kernel<128>,
+                       dim3(g.n_heads, batch), dim3(128), 0, s, o, g.n_heads, ctx_lens,
+                       static_cast<const float*>(workspace), ws_splits, split_tokens));
   note_launch();
   }
   return TK_OK;

@@ -304,6 +304,18 @@ struct tk_instance {
   };
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> ev_pool;
+  // Decode steps as CUDA graphs (tk_decode_step): one graph per (padded batch, context
+  // bucket); every per-step input lives at fixed device addresses (dec_fixed), padding
+  // rows attend to a scratch page past the pool (page kv_pages).
+  struct DecGraph {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;  // kernels in the graph (tk_launch_count)
+    int seen = 0;
+    bool failed = false;
+  };
+  std::map<uint64_t, DecGraph> dec_graphs;
+  uint8_t* dec_fixed = nullptr;
+  int64_t dec_fixed_bytes = 0;
 };
 
 namespace tk {
@@ -573,9 +585,10 @@ int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed
   inst->page_bytes = static_cast<int64_t>(inst->geom.page_elems()) * 2;
   inst->max_chunk = max_chunk;
   if (kv_pages > 0) {
-    TK_CUDA(cudaMalloc(&inst->pool, inst->page_bytes * kv_pages));
+    // one page past the pool: the K/V of padding rows of graph decode steps
+    TK_CUDA(cudaMalloc(&inst->pool, inst->page_bytes * (kv_pages + 1)));
     // stale slots are read (and masked) by whole-page loads: keep them finite
-    TK_CUDA(cudaMemset(inst->pool, 0, inst->page_bytes * kv_pages));
+    TK_CUDA(cudaMemset(inst->pool, 0, inst->page_bytes * (kv_pages + 1)));
   }
   TK_CUDA(cudaStreamCreateWithFlags(&inst->s_compute, cudaStreamNonBlocking));
   TK_CUDA(cudaStreamCreateWithFlags(&inst->s_copy, cudaStreamNonBlocking));
@@ -610,6 +623,8 @@ int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed
   inst->dec_ws_bytes = decode_attention_workspace_bytes(max_chunk, m.n_heads, m.head_dim,
                                                         std::min(inst->dec_max_ctx, 1 << 16));
   TK_CUDA(cudaMalloc(&inst->dec_ws, inst->dec_ws_bytes));
+  inst->dec_fixed_bytes = kSlotBytes;
+  TK_CUDA(cudaMalloc(&inst->dec_fixed, inst->dec_fixed_bytes));
   TK_CUDA(cudaMalloc(&inst->attn_partial, attn_partial_bytes(m.n_heads, m.head_dim)));
   // zeroed once: the attention kernel's per-group arrival counters live at its end
   TK_CUDA(cudaMemset(inst->attn_partial, 0, attn_partial_bytes(m.n_heads, m.head_dim)));
@@ -638,6 +653,9 @@ int tk_instance_destroy(tk_instance* inst) {
     cudaFree(s.dev);
     cudaEventDestroy(s.done);
   }
+  for (auto& kv : inst->dec_graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  cudaFree(inst->dec_fixed);
   cudaFree(inst->pool);
   cudaFree(inst->resid);
   cudaFree(inst->delta);
@@ -869,6 +887,44 @@ int tk_prefill_chunk(tk_instance* inst, int32_t n_tokens, const int32_t* token_i
 }
 
 // ------------------------------------------------------------------ decode step
+// The device work of one decode step over `batch` rows whose inputs sit at the given
+// device addresses: embed, every layer (KV append, split-KV paged attention, GEMMs),
+// head + argmax.  Run eagerly, or recorded once per shape bucket into a CUDA graph.
+static int decode_body(tk_instance* inst, cudaStream_t s, int batch, const int32_t* ids_d,
+                       const TokenMeta* meta_d, const int32_t* lens_d, const int32_t* bt_d,
+                       int bt_stride, const int32_t* rows_d, int32_t* out_d, int max_ctx,
+                       double attn_flops, double attn_bytes) {
+  const tk_model_desc& m = inst->w->md;
+  const int h = m.hidden;
+  int rc = m.arch == TK_ARCH_OPT
+               ? launch_embed_opt(ids_d, meta_d, batch, inst->w->embed, inst->w->pos, inst->resid, h, s)
+               : launch_embed_llama(ids_d, batch, inst->w->embed, inst->resid, h, s);
+  if (rc) return rc;
+  const float scale = attn_scale(m);
+  for (int l = 0; l < m.n_layers; ++l) {
+    rc = run_layer(inst, l, batch, meta_d, s, attn_flops, attn_bytes, [&]() {
+      return launch_decode_attention(inst->qkv, 3 * h, inst->attn, inst->pool, inst->geom, l, bt_d,
+                                     bt_stride, lens_d, batch, max_ctx, scale, inst->dec_ws,
+                                     inst->dec_ws_bytes, s);
+    });
+    if (rc) return rc;
+  }
+  return run_head(inst, batch, rows_d, out_d, s);
+}
+
+static bool decode_graphs_on() {
+  static const bool on = getenv("TK_NO_DECODE_GRAPH") == nullptr;
+  return on;
+}
+
+// Graph batch bucket: the skinny GEMM's batch widths (16/32/64/128), then steps of 32.
+static int decode_batch_bucket(int batch, int cap) {
+  int b = 16;
+  while (b < batch && b < 128) b *= 2;
+  if (batch > 128) b = (batch + 31) / 32 * 32;
+  return std::min(std::max(b, batch), cap);
+}
+
 int tk_decode_step(tk_instance* inst, int32_t batch, const int32_t* last_tokens,
                    const int32_t* ctx_lens, const int32_t* block_tables, int32_t bt_stride,
                    int32_t* next_tokens_out, float* logits_out, tk_event** ev_out) {
@@ -879,25 +935,9 @@ int tk_decode_step(tk_instance* inst, int32_t batch, const int32_t* last_tokens,
   TK_CHECK(m.n_labels == 0, TK_EUNSUPPORTED, "tk_decode_step: classifier instance");
   TK_CUDA(cudaSetDevice(inst->device));
   cudaStream_t s = inst->s_compute;
-  Slot* slot;
-  int rc = take_slot(inst, &slot);
-  if (rc) return rc;
-  Packer pk{slot};
   const int pt = inst->geom.page_tokens;
-  int32_t* ids_d;
-  pk.put(last_tokens, batch, &ids_d);
-  TokenMeta* meta_d;
-  TokenMeta* meta = pk.put<TokenMeta>(nullptr, batch, &meta_d);
-  int32_t* lens_d;
-  int32_t* lens = pk.put<int32_t>(nullptr, batch, &lens_d);
-  int32_t* bt_d;
-  pk.put(block_tables, static_cast<int64_t>(batch) * bt_stride, &bt_d);
-  int32_t* rows_d;
-  int32_t* rows = pk.put<int32_t>(nullptr, batch, &rows_d);
-  int32_t* out_d;
-  int32_t* out_h = pk.put<int32_t>(nullptr, batch, &out_d);
-  TK_CHECK(pk.ok(), TK_EINVAL, "tk_decode_step: metadata exceeds staging slot");
   int max_ctx = 0;
+  double kv_sum = 0;
   for (int b = 0; b < batch; ++b) {
     const int ctx = ctx_lens[b];
     TK_CHECK(ctx >= 0 && (ctx / pt) < bt_stride, TK_EINVAL, "tk_decode_step: ctx beyond block table");
@@ -906,41 +946,133 @@ int tk_decode_step(tk_instance* inst, int32_t batch, const int32_t* last_tokens,
     TK_CHECK(last_tokens[b] >= 0 && last_tokens[b] < m.vocab, TK_EINVAL, "tk_decode_step: token");
     const int page = block_tables[static_cast<int64_t>(b) * bt_stride + ctx / pt];
     TK_CHECK(page >= 0 && page < inst->kv_pages, TK_ECAPACITY, "tk_decode_step: page out of pool");
-    meta[b] = TokenMeta{ctx, page, ctx % pt, b};
-    lens[b] = ctx + 1;
-    rows[b] = b;
     max_ctx = std::max(max_ctx, ctx + 1);
+    kv_sum += ctx + 1;
   }
   TK_CHECK(decode_attention_workspace_bytes(batch, m.n_heads, m.head_dim, max_ctx) <=
                inst->dec_ws_bytes,
            TK_EINVAL, "tk_decode_step: context exceeds attention workspace");
-  tk_event* ev;
-  rc = new_event(inst, s, &ev);
-  if (rc) return rc;
-  TK_CUDA(cudaMemcpyAsync(slot->dev, slot->host, pk.off, cudaMemcpyHostToDevice, s));
-  inst->last_h2d = pk.off;
-  inst->last_d2h = static_cast<int64_t>(batch) * 4;
-  const int h = m.hidden;
-  rc = m.arch == TK_ARCH_OPT
-           ? launch_embed_opt(ids_d, meta_d, batch, inst->w->embed, inst->w->pos, inst->resid, h, s)
-           : launch_embed_llama(ids_d, batch, inst->w->embed, inst->resid, h, s);
-  if (rc) return rc;
-  const float scale = attn_scale(m);
-  double kv_sum = 0;
-  for (int b = 0; b < batch; ++b) kv_sum += ctx_lens[b] + 1;
   const double attn_flops = 4.0 * m.head_dim * m.n_heads * kv_sum;
   // K and V of every attended token read once, Q read, O written (one layer)
   const double attn_bytes = kv_sum * 2.0 * m.hidden * 2 + 2.0 * batch * m.hidden * 2;
-  for (int l = 0; l < m.n_layers; ++l) {
-    rc = run_layer(inst, l, batch, meta_d, s, attn_flops, attn_bytes, [&]() {
-      return launch_decode_attention(inst->qkv, 3 * h, inst->attn, inst->pool, inst->geom, l, bt_d,
-                                     bt_stride, lens_d, batch, max_ctx, scale, inst->dec_ws,
-                                     inst->dec_ws_bytes, s);
-    });
-    if (rc) return rc;
+
+  // Graph mode: the step padded to a batch bucket and a context bucket (1024 tokens),
+  // inputs copied to fixed device addresses; padding rows are token 0 at position 0
+  // whose K/V go to the scratch page and whose outputs are dropped.
+  bool graph = decode_graphs_on() && !inst->prof && logits_out == nullptr && inst->kv_pages > 0;
+  int rows_p = batch, ctx_p = max_ctx, stride_p = bt_stride;
+  if (graph) {
+    rows_p = decode_batch_bucket(batch, inst->max_chunk);
+    ctx_p = std::max(max_ctx, std::min((max_ctx + 1023) / 1024 * 1024, inst->dec_max_ctx));
+    if (decode_attention_workspace_bytes(rows_p, m.n_heads, m.head_dim, ctx_p) > inst->dec_ws_bytes)
+      ctx_p = max_ctx;
+    stride_p = (ctx_p + pt - 1) / pt;
+    graph = decode_attention_workspace_bytes(rows_p, m.n_heads, m.head_dim, ctx_p) <=
+            inst->dec_ws_bytes;
   }
-  rc = run_head(inst, batch, rows_d, out_d, s);
+  if (!graph) {
+    rows_p = batch;
+    ctx_p = max_ctx;
+    stride_p = bt_stride;
+  }
+  Slot* slot;
+  int rc = take_slot(inst, &slot);
   if (rc) return rc;
+  Packer pk{slot};
+  int32_t* ids_d;
+  int32_t* ids = pk.put<int32_t>(nullptr, rows_p, &ids_d);
+  TokenMeta* meta_d;
+  TokenMeta* meta = pk.put<TokenMeta>(nullptr, rows_p, &meta_d);
+  int32_t* lens_d;
+  int32_t* lens = pk.put<int32_t>(nullptr, rows_p, &lens_d);
+  int32_t* rows_d;
+  int32_t* rows = pk.put<int32_t>(nullptr, rows_p, &rows_d);
+  int32_t* bt_d;
+  int32_t* bt = pk.put<int32_t>(nullptr, static_cast<int64_t>(rows_p) * stride_p, &bt_d);
+  const int64_t in_bytes = pk.off;
+  int32_t* out_d;
+  int32_t* out_h = pk.put<int32_t>(nullptr, rows_p, &out_d);
+  TK_CHECK(pk.ok() && pk.off <= inst->dec_fixed_bytes, TK_EINVAL,
+           "tk_decode_step: metadata exceeds staging slot");
+  const int trash = inst->kv_pages;  // the page past the pool (graph padding rows)
+  for (int b = 0; b < rows_p; ++b) {
+    int32_t* row_bt = bt + static_cast<int64_t>(b) * stride_p;
+    if (b < batch) {
+      const int ctx = ctx_lens[b];
+      const int32_t* src = block_tables + static_cast<int64_t>(b) * bt_stride;
+      const int ncopy = std::min(bt_stride, stride_p);
+      memcpy(row_bt, src, static_cast<size_t>(ncopy) * 4);
+      for (int j = ncopy; j < stride_p; ++j) row_bt[j] = src[0];  // never read (ctx bound)
+      ids[b] = last_tokens[b];
+      meta[b] = TokenMeta{ctx, src[ctx / pt], ctx % pt, b};
+      lens[b] = ctx + 1;
+    } else {
+      for (int j = 0; j < stride_p; ++j) row_bt[j] = trash;
+      ids[b] = 0;
+      meta[b] = TokenMeta{0, trash, 0, b};
+      lens[b] = 1;
+    }
+    rows[b] = b;
+  }
+  tk_event* ev;
+  rc = new_event(inst, s, &ev);
+  if (rc) return rc;
+  inst->last_h2d = in_bytes;
+  inst->last_d2h = static_cast<int64_t>(batch) * 4;
+  if (!graph) {
+    TK_CUDA(cudaMemcpyAsync(slot->dev, slot->host, in_bytes, cudaMemcpyHostToDevice, s));
+    rc = decode_body(inst, s, batch, ids_d, meta_d, lens_d, bt_d, stride_p, rows_d, out_d,
+                     max_ctx, attn_flops, attn_bytes);
+    if (rc) return rc;
+  } else {
+    auto fixed = [&](auto* p) {
+      return reinterpret_cast<decltype(p)>(inst->dec_fixed +
+                                           (reinterpret_cast<uint8_t*>(p) - slot->dev));
+    };
+    TK_CUDA(cudaMemcpyAsync(inst->dec_fixed, slot->host, in_bytes, cudaMemcpyHostToDevice, s));
+    const int32_t* fids = fixed(ids_d);
+    const TokenMeta* fmeta = fixed(meta_d);
+    const int32_t* flens = fixed(lens_d);
+    const int32_t* frows = fixed(rows_d);
+    const int32_t* fbt = fixed(bt_d);
+    out_d = fixed(out_d);
+    auto body = [&]() {
+      return decode_body(inst, s, rows_p, fids, fmeta, flens, fbt, stride_p, frows, out_d, ctx_p,
+                         attn_flops, attn_bytes);
+    };
+    const uint64_t key = (static_cast<uint64_t>(rows_p) << 32) | static_cast<uint32_t>(ctx_p);
+    auto& g = inst->dec_graphs[key];
+    if (g.exec) {
+      TK_CUDA(cudaGraphLaunch(g.exec, s));
+      g_launches.fetch_add(g.launches, std::memory_order_relaxed);
+    } else if (g.failed || g.seen++ == 0) {
+      // first use of a shape: eager (sets kernel attributes, plans, tensor maps)
+      rc = body();
+      if (rc) return rc;
+    } else {
+      const int64_t l0 = g_launches.load();
+      TK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      rc = body();
+      cudaGraph_t cg = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(s, &cg);
+      const int64_t n = g_launches.load() - l0;
+      g_launches.fetch_sub(n, std::memory_order_relaxed);  // recorded, not run
+      cudaError_t ie = cudaErrorUnknown;
+      if (rc == TK_OK && e == cudaSuccess && cg) ie = cudaGraphInstantiate(&g.exec, cg, 0);
+      if (cg) cudaGraphDestroy(cg);
+      if (ie != cudaSuccess) {
+        cudaGetLastError();
+        g.exec = nullptr;
+        g.failed = true;  // this shape stays eager
+        rc = body();
+        if (rc) return rc;
+      } else {
+        g.launches = n;
+        TK_CUDA(cudaGraphLaunch(g.exec, s));
+        g_launches.fetch_add(n, std::memory_order_relaxed);
+      }
+    }
+  }
   TK_CUDA(cudaMemcpyAsync(out_h, out_d, batch * 4, cudaMemcpyDeviceToHost, s));
   TK_CUDA(cudaEventRecord(ev->end, s));
   TK_CUDA(cudaEventRecord(slot->done, s));

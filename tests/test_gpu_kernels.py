@@ -168,10 +168,13 @@ def _decode_case(ctxs, seed, H=8, L=3, D=128, pt=16):
     return pool, bt, tables, q, perm[cur:]
 
 
-@pytest.mark.parametrize("ctxs", [[1], [16, 17, 300], [1000, 4097, 40, 2048, 9000],
-                                  [8192, 3000, 10240, 511]])
-def test_paged_decode_attention(ctxs):
-    L, H, D, pt, layer = 3, 8, 128, 16, 1
+@pytest.mark.parametrize("ctxs,D", [([1], 128), ([16, 17, 300], 128),
+                                    ([1000, 4097, 40, 2048, 9000], 128),
+                                    ([8192, 3000, 10240, 511], 128),
+                                    ([1, 33, 300], 64), ([1000, 4097, 40, 2048], 64)])
+def test_paged_decode_attention(ctxs, D):
+    """head_dim 64 is the OPT-125M tiny decoder (BASELINE.json configs[0])."""
+    L, H, pt, layer = 3, 8, 16, 1
     pool, bt, tables, q, spare = _decode_case(ctxs, len(ctxs) * 7 + ctxs[0], H, L, D, pt)
     lens = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
     o = native.paged_decode_attention(q, pool, layer, L, bt.cuda(), lens, pt)

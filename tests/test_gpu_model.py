@@ -46,7 +46,12 @@ def _plan(lens, chunk_size):
     return reqs, tables, nxt, chunkify(reqs, chunk_size)
 
 
-@pytest.mark.parametrize("model", [native.TINY_OPT, native.TINY_LLAMA])
+# OPT-125M width (head_dim 64: the tiny decoder of BASELINE.json configs[0]), 2 layers
+OPT125_2L = native.ModelShape("opt125m-2l", native.TK_ARCH_OPT, 2, 768, 12, 3072, 50272,
+                              max_positions=2048)
+
+
+@pytest.mark.parametrize("model", [native.TINY_OPT, native.TINY_LLAMA, OPT125_2L])
 @pytest.mark.parametrize("lens", [[18, 100, 512, 900], [18, 100, 512 + 7, 900, 5]])
 def test_prefill_and_decode_match_oracle(model, lens):
     """The reference's prompt lengths (pkg/tests/test_prefill.py:58-67) and a
@@ -202,3 +207,54 @@ def test_kv_send_many_scattered_pages_and_swap_round_trip():
     finally:
         native.host_free(h_in), native.host_free(h_out)
         p.close(), d.close()
+
+
+@pytest.mark.parametrize("model", [native.TINY_OPT, native.TINY_LLAMA, OPT125_2L])
+def test_decode_graph_steps_match_eager(model):
+    """tk_decode_step records each (padded batch, 1024-token context bucket) shape
+    into a CUDA graph on its second use and replays it afterwards.  Each graph-mode
+    step (first use eager, second captured, later replayed; batch 5 padded to 16 rows
+    whose K/V land on the scratch page) is followed by the same step through the
+    eager logits path at the same positions: tokens must agree wherever the eager
+    logits have a top-1/top-2 margin above 1e-3 of the row's range, and the KV the
+    two paths wrote must agree to bf16 rounding."""
+    lens = [40, 300, 17, 520, 5]
+    reqs, tables, n_pages, chunks = _plan(lens, 512)
+    inst = native.Instance(model, device=0, seed=9, kv_pages=n_pages, page_tokens=PT, max_chunk=512)
+    prompts = {r.id: token_ids_for(r, model.vocab, seed=2) for r in reqs}
+    for chunk in chunks:
+        ids, slices, bt = [], [], []
+        for rid, start, n in chunk.slices:
+            ids += prompts[rid][start:start + n]
+            slices.append((start, n, len(bt), len(tables[rid]), int(start + n == lens[rid])))
+            bt += tables[rid]
+        inst.prefill_chunk(ids, slices, bt)[0].wait()
+    stride = max(len(t) for t in tables.values())
+    bt = sum((tables[i] + [tables[i][0]] * (stride - len(tables[i])) for i in range(len(lens))), [])
+    last = [7, 8, 9, 10, 11]
+    checked = 0
+    for step in range(5):
+        ctx = [n + step for n in lens]
+        ev, toks = inst.decode_step(last, ctx, bt, stride)
+        ev.wait()
+        g_toks = list(toks)
+        kv_g = [inst.read_page(tables[i][c // PT]) for i, c in enumerate(ctx)]
+        ev, e_toks, logits = inst.decode_step(last, ctx, bt, stride, want_logits=True)
+        ev.wait()
+        kv_e = [inst.read_page(tables[i][c // PT]) for i, c in enumerate(ctx)]
+        # the stream-K GEMMs sum split-tile partials in arrival order, so a recomputed
+        # step may differ in the last bf16 bit; anything larger is a graph bug
+        for a, b in zip(kv_g, kv_e):
+            fa, fb = bf16_bits_to_f32(a), bf16_bits_to_f32(b)
+            assert (fa - fb).abs().max().item() <= 2e-2 * max(1e-6, fb.abs().max().item())
+        lg = torch.from_numpy(logits)
+        top2 = lg.topk(2, dim=-1).values
+        span = lg.max(-1).values - lg.min(-1).values
+        decided = (top2[:, 0] - top2[:, 1]) > 1e-3 * span
+        for i in range(len(lens)):
+            if decided[i]:
+                assert g_toks[i] == int(e_toks[i]), (step, i)
+                checked += 1
+        last = [int(t) for t in e_toks]
+    assert checked >= 15
+    inst.close()
