@@ -477,8 +477,13 @@ def decode_run(args, shape, device: int, peaks: dict, configs=((32, 2048), (128,
             ev, _ = inst.decode_step(last, [ctx + i] * batch, bt, pages_per)
             ev.wait()
         # timed without per-kernel events, then a profiled pass for the breakdown
-        evs = [inst.decode_step(last, [ctx + 3 + i] * batch, bt, pages_per)[0]
-               for i in range(steps)]
+        evs, t_call = [], []
+        for i in range(steps):
+            t_host = time.perf_counter()
+            evs.append(inst.decode_step(last, [ctx + 3 + i] * batch, bt, pages_per)[0])
+            t_call.append(time.perf_counter() - t_host)
+        # host cost of one call: the first calls only (later ones wait for a staging slot)
+        host_us = sorted(t_call[:6])[3] * 1e6
         ns = native.event_elapsed_ns(evs[0], evs[-1])
         inst.profile(True)
         pevs = [inst.decode_step(last, [ctx + 3 + i] * batch, bt, pages_per)[0]
@@ -498,6 +503,8 @@ def decode_run(args, shape, device: int, peaks: dict, configs=((32, 2048), (128,
                                    "frac": round(gbs / peaks["hbm_gbs"], 4),
                                    "launches": att["launches"]},
             "gemm_weight_stream_gbs": round(gemm_bytes / (gemm_ms / 1e3) / 1e9, 1),
+            "host_enqueue_us_per_step": round(host_us, 1),
+            "cuda_graph": not os.environ.get("TK_NO_DECODE_GRAPH"),
             "share_of_step": {k: round(v["ms"] / (pns / 1e6), 4) for k, v in prof.items()},
         }
     return out
