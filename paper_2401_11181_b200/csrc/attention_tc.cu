@@ -179,10 +179,22 @@ __device__ __forceinline__ UnitView unit_view(const FaParams& p, int u) {
   return v;
 }
 
-template <int POLY, bool LD_BATCH, int EXP = 0, int DEG = 5>
+// D = head_dim: 128 (OPT-13B, Llama-2-7B) or 64 (the OPT-125M-class length
+// predictor and tiny decoder): a 64-wide head is one SW128 atom column of Q/K/V,
+// so its S MMA is K=64 (4 UMMAs) and O_t uses 64 TMEM columns; the K/V ring
+// keeps the same 128 KB as 8 entries of 16 KB.
+template <int D, int POLY, bool LD_BATCH, int EXP = 0, int DEG = 5>
 __global__ void __launch_bounds__(kThreads, 1)
     chunk_attn_fa_kernel(const __grid_constant__ CUtensorMap tmap_q,
                          const __grid_constant__ CUtensorMap tmap_kv, const FaParams p) {
+  static_assert(D == 128 || D == 64, "tcgen05 attention: head_dim 128 or 64");
+  constexpr int kD = D;                          // (shadow the 128-wide defaults)
+  constexpr int kHalves = D / 64;                // 64-wide SW128 atom columns
+  constexpr int kQTile = kRows * D * 2;
+  constexpr int kQHalf = kRows * 128;            // stride between Q atom columns
+  constexpr int kEntry = kHalves * kKvHalf;
+  constexpr int kRing = (4 * 2 * kKvHalf) / kEntry;
+  constexpr int kPartRowBytes = D * 2 + 16;
   griddep_launch();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -244,19 +256,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool two = v.pr.nrows1 > 0;
         mbar_expect_tx(q_full, two ? 2 * kQTile : kQTile);
         for (int t = 0; t < (two ? 2 : 1); ++t)
-          for (int h = 0; h < 2; ++h)
+          for (int h = 0; h < kHalves; ++h)
             tma_load_2d(sQ + t * kQTile + h * kQHalf, &tmap_q, q_full, v.head * kD + h * 64,
                         v.pr.row0 + t * kRows, pol_q);
       }
-      const int i = (lane >> 1) & 7, h = lane & 1;
+      // lanes 0 .. 8*kHalves-1: page i of the block's 8, d-half h
+      const int i = (lane / kHalves) & 7, h = lane % kHalves;
+      constexpr int kLoadLanes = 8 * kHalves;
       auto page_of = [&](int kb) {
         const int pi = kb * (kKeys / 16) + i;
         return pi < sl.n_pages ? __ldg(pages + pi) : __ldg(pages);  // beyond: masked keys
       };
-      int pg_next = lane < 16 ? page_of(v.kb0) : 0;
+      int pg_next = lane < kLoadLanes ? page_of(v.kb0) : 0;
       for (int j = 0; j < v.nblk; ++j) {
         const int pg = pg_next;
-        if (lane < 16 && j + 1 < v.nblk) pg_next = page_of(EXP == 2 ? v.kb0 : v.kb0 + j + 1);
+        if (lane < kLoadLanes && j + 1 < v.nblk) pg_next = page_of(EXP == 2 ? v.kb0 : v.kb0 + j + 1);
 #pragma unroll
         for (int kv = 0; kv < 2; ++kv, ++ent) {
           const int st = ent % kRing;
@@ -266,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (EXP >= 3) fa_stamp(5 + kv, 0, ent / 2);
           }
           __syncwarp();
-          if (lane < 16) {
+          if (lane < kLoadLanes) {
             const int blk = ((pg * p.n_layers + p.layer) * p.n_heads + v.head) * 2 + kv;
             tma_load_2d(sKV + st * kEntry + h * kKvHalf + i * 16 * 128, &tmap_kv, &kv_full[st],
                         h * 64, blk * 16, pol_kv);
@@ -299,8 +313,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto issue_s = [&](int t, uint32_t k_addr) {
         if (elect_one_sync()) {
-          umma_bf16_k128<kQHalf / 16, kKvHalf / 16>(tmem + t * 128, q_desc[t],
-                                                     umma_desc_sw128(k_addr), idesc_s, 0u);
+          if constexpr (D == 128)
+            umma_bf16_k128<kQHalf / 16, kKvHalf / 16>(tmem + t * 128, q_desc[t],
+                                                       umma_desc_sw128(k_addr), idesc_s, 0u);
+          else
+            umma_bf16_k64(tmem + t * 128, q_desc[t], umma_desc_sw128(k_addr), idesc_s, 0u);
           umma_commit(&s_full[t]);
         }
         __syncwarp();
@@ -577,10 +594,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Merge the pieces of every split (pair, head): half a warp per query row, each
 // lane 8 of the 128 dims (16-byte bf16 loads); up to 4 pieces are loaded at once (one
 // round trip for the usual 2-3), partial rows read coalesced (256 B per piece-row).
+template <int D>
 __global__ void __launch_bounds__(256)
     fa_combine_kernel(__nv_bfloat16* __restrict__ o, const FaPair* __restrict__ pairs,
                       const FaGroup* __restrict__ groups, int n_heads,
                       const float* __restrict__ partial) {
+  constexpr int kD = D;
+  constexpr int kPartRowBytes = D * 2 + 16;
   griddep_launch();
   griddep_wait();  // partials of the attention kernel
   const FaGroup g = groups[blockIdx.x >> 4];
@@ -588,7 +608,7 @@ __global__ void __launch_bounds__(256)
   const FaPair pr = pairs[g.pair];
   const int nrows = t ? pr.nrows1 : pr.nrows0;
   const int r = rg * 16 + static_cast<int>(threadIdx.x >> 4), lane = threadIdx.x & 15;
-  if (r >= nrows) return;
+  if (r >= nrows || lane >= kD / 8) return;  // D=64: 8 lanes per row
   auto row_of = [&](int x) {
     return reinterpret_cast<const uint8_t*>(partial) +
            ((static_cast<size_t>(g.first_piece + x) * 2 + t) * kRows + r) * kPartRowBytes;
@@ -732,32 +752,34 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
                               const int32_t* cta_off_dev, const tk_slice* slices_dev,
                               const int32_t* bt_dev, float scale, float* partial,
                               cudaStream_t s) {
-  TK_CHECK(g.head_dim == kD, TK_EUNSUPPORTED, "tcgen05 attention: head_dim 128");
+  TK_CHECK(g.head_dim == 128 || g.head_dim == 64, TK_EUNSUPPORTED,
+           "tcgen05 attention: head_dim 128 or 64");
   TK_CHECK(g.page_tokens == 16, TK_EUNSUPPORTED, "tcgen05 attention: 16-token pages");
   if (plan.n_units == 0) return TK_OK;
   CUtensorMap tq, tkv;
   int rc = make_tmap_kmajor(&tq, qkv, q_rows, q_stride, kRows);
   if (rc) return rc;
   const uint64_t blocks = static_cast<uint64_t>(pool_pages) * g.n_layers * g.n_heads * 2;
-  rc = make_tmap_kmajor(&tkv, pool, blocks * g.page_tokens, kD, g.page_tokens);
+  rc = make_tmap_kmajor(&tkv, pool, blocks * g.page_tokens, g.head_dim, g.page_tokens);
   if (rc) return rc;
   // TK_FA_VARIANT (experiments): 0 degree-3 poly for 1/4 of the exponentials
   // (default), 1 MUFU only, 2 poly 1/2,
   // 3 poly 1/4 with one wait for the four S loads, 4 MUFU only + batched loads
   static const int variant = getenv("TK_FA_VARIANT") ? atoi(getenv("TK_FA_VARIANT")) : 0;
   using KernFn = void (*)(CUtensorMap, CUtensorMap, FaParams);
-  KernFn kern = variant == 1 ? (KernFn)chunk_attn_fa_kernel<0, false>
-              : variant == 2 ? (KernFn)chunk_attn_fa_kernel<2, false>
-              : variant == 3 ? (KernFn)chunk_attn_fa_kernel<4, true>
-              : variant == 4 ? (KernFn)chunk_attn_fa_kernel<0, true>
-              : variant == 5 ? (KernFn)chunk_attn_fa_kernel<4, false, 1>
-              : variant == 6 ? (KernFn)chunk_attn_fa_kernel<4, false, 2>
-              : variant == 7 ? (KernFn)chunk_attn_fa_kernel<4, false, 3>
-              : variant == 8 ? (KernFn)chunk_attn_fa_kernel<4, false, 4>
-              : variant == 9 ? (KernFn)chunk_attn_fa_kernel<4, false, 0, 3>
-              : variant == 10 ? (KernFn)chunk_attn_fa_kernel<3, false, 0, 3>
-              : variant == 11 ? (KernFn)chunk_attn_fa_kernel<2, false, 0, 3>
-                             : (KernFn)chunk_attn_fa_kernel<4, false, 0, 3>;
+  KernFn kern = g.head_dim == 64 ? (KernFn)chunk_attn_fa_kernel<64, 4, false, 0, 3>
+              : variant == 1 ? (KernFn)chunk_attn_fa_kernel<128, 0, false>
+              : variant == 2 ? (KernFn)chunk_attn_fa_kernel<128, 2, false>
+              : variant == 3 ? (KernFn)chunk_attn_fa_kernel<128, 4, true>
+              : variant == 4 ? (KernFn)chunk_attn_fa_kernel<128, 0, true>
+              : variant == 5 ? (KernFn)chunk_attn_fa_kernel<128, 4, false, 1>
+              : variant == 6 ? (KernFn)chunk_attn_fa_kernel<128, 4, false, 2>
+              : variant == 7 ? (KernFn)chunk_attn_fa_kernel<128, 4, false, 3>
+              : variant == 8 ? (KernFn)chunk_attn_fa_kernel<128, 4, false, 4>
+              : variant == 9 ? (KernFn)chunk_attn_fa_kernel<128, 4, false, 0, 3>
+              : variant == 10 ? (KernFn)chunk_attn_fa_kernel<128, 3, false, 0, 3>
+              : variant == 11 ? (KernFn)chunk_attn_fa_kernel<128, 2, false, 0, 3>
+                             : (KernFn)chunk_attn_fa_kernel<128, 4, false, 0, 3>;
   TK_SMEM_OPT_IN(kern, kSmem);
   FaParams prm;
   prm.pairs = pairs_dev;
@@ -775,8 +797,9 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   TK_CUDA(cudaGetLastError());
   note_launch();
   if (plan.n_groups > 0) {
-    TK_CUDA(launch_pdl(fa_combine_kernel, dim3(plan.n_groups * 16), dim3(256), 0, s, o,
-                       pairs_dev, groups_dev, g.n_heads, partial));
+    TK_CUDA(launch_pdl(g.head_dim == 64 ? fa_combine_kernel<64> : fa_combine_kernel<128>,
+                       dim3(plan.n_groups * 16), dim3(256), 0, s, o, pairs_dev, groups_dev,
+                       g.n_heads, partial));
     TK_CUDA(cudaGetLastError());
     note_launch();
   }

@@ -29,7 +29,7 @@ static thread_local std::string g_err;
 
 bool use_tc_attention(int head_dim) {
   static const bool forced_off = getenv("TK_ATTN_MMA_SYNC") != nullptr;
-  return head_dim == 128 && !forced_off;
+  return (head_dim == 128 || head_dim == 64) && !forced_off;
 }
 static std::atomic<int64_t> g_launches{0};
 

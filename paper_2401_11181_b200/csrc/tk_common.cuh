@@ -426,6 +426,24 @@ __device__ __forceinline__ void umma_bf16_k128(uint32_t d_tmem, uint64_t a_desc,
       : "memory");
 }
 
+// Four K=16 UMMAs over a 64-deep K-major SW128 panel (one atom column: +32 bytes,
+// 2 descriptor units, per step), e.g. S = Q K^T for head_dim 64.
+__device__ __forceinline__ void umma_bf16_k64(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 a, b;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.s64 a, %1, 2;\n\tadd.s64 b, %2, 2;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 4;\n\tadd.s64 b, %2, 4;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 6;\n\tadd.s64 b, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Eight K=16 UMMAs with A in tensor memory (+8 columns per step: 16 bf16 packed
 // two per column) and B an MN-major SW128 operand advancing 16 rows (2 KB,
 // 128 descriptor units) per step.

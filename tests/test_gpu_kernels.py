@@ -260,16 +260,21 @@ def test_chunk_attention_mixed_slices():
     print(f"chunk attention mixed: max rel {worst[0]:.2e}, min cos {worst[1]:.6f}")
 
 
-@pytest.mark.parametrize("prefix,n,H", [(0, 512, 40), (2048, 512, 40), (3000, 512, 40),
-                                        (4096, 512, 40), (7680, 512, 8), (130, 77, 40),
-                                        (256, 300, 3)])
-def test_chunk_attention_long_prefix_pieces(prefix, n, H):
+@pytest.mark.parametrize("prefix,n,H,D", [(0, 512, 40, 128), (2048, 512, 40, 128),
+                                          (3000, 512, 40, 128), (4096, 512, 40, 128),
+                                          (7680, 512, 8, 128), (130, 77, 40, 128),
+                                          (256, 300, 3, 128),
+                                          # head_dim 64: the OPT-125M-class predictor /
+                                          # tiny decoder on the same tcgen05 kernel
+                                          (0, 512, 12, 64), (2048, 512, 12, 64),
+                                          (130, 77, 12, 64), (1000, 300, 5, 64)])
+def test_chunk_attention_long_prefix_pieces(prefix, n, H, D):
     """One slice over a long paged prefix (the C2 regime: 2k-8k prompts in 512
     chunks): the stream-K plan cuts (head, tile pair) work into pieces merged by
     the combine kernel; unaligned starts and lone tiles.  Every head is checked,
     with negative controls (shifted mask, and a dropped 128-key block on the
     device)."""
-    L, D, pt, layer = 2, 128, 16, 0
+    L, pt, layer = 2, 16, 0
     pool, bt, slices, qkv, spare = _chunk_case([(prefix, n)], H, prefix + n, L, D, pt)
     o = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bt, pt)
     torch.cuda.synchronize()
