@@ -767,8 +767,7 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   // 3 poly 1/4 with one wait for the four S loads, 4 MUFU only + batched loads
   static const int variant = getenv("TK_FA_VARIANT") ? atoi(getenv("TK_FA_VARIANT")) : 0;
   using KernFn = void (*)(CUtensorMap, CUtensorMap, FaParams);
-  KernFn kern = g.head_dim == 64 ? (KernFn)chunk_attn_fa_kernel<64, 4, false, 0, 3>
-              : variant == 1 ? (KernFn)chunk_attn_fa_kernel<128, 0, false>
+  KernFn kern = variant == 1 ? (KernFn)chunk_attn_fa_kernel<128, 0, false>
               : variant == 2 ? (KernFn)chunk_attn_fa_kernel<128, 2, false>
               : variant == 3 ? (KernFn)chunk_attn_fa_kernel<128, 4, true>
               : variant == 4 ? (KernFn)chunk_attn_fa_kernel<128, 0, true>
@@ -780,7 +779,13 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
               : variant == 10 ? (KernFn)chunk_attn_fa_kernel<128, 3, false, 0, 3>
               : variant == 11 ? (KernFn)chunk_attn_fa_kernel<128, 2, false, 0, 3>
                              : (KernFn)chunk_attn_fa_kernel<128, 4, false, 0, 3>;
-  TK_SMEM_OPT_IN(kern, kSmem);
+  if (g.head_dim == 64) {
+    // its own opt-in site: TK_SMEM_OPT_IN keeps one per-device flag per call site
+    kern = chunk_attn_fa_kernel<64, 4, false, 0, 3>;
+    TK_SMEM_OPT_IN(kern, kSmem);
+  } else {
+    TK_SMEM_OPT_IN(kern, kSmem);
+  }
   FaParams prm;
   prm.pairs = pairs_dev;
   prm.units = units_dev;

@@ -609,10 +609,30 @@ __device__ __forceinline__ void skinny_store(const GemmArgs& p, int n, int m0, c
   // v[j] = D[n, m0 + j]: output feature n of batch row m0 + j
   if (n >= p.N) return;
   float b = 0.f;
-  if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_RELU || EPI == EPI_F32_BIAS_RESID) {
+  if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_RELU || EPI == EPI_F32_BIAS_RESID ||
+                EPI == EPI_QKV_PAGED) {
     if (p.bias != nullptr) b = __bfloat162float(p.bias[n]);
   }
   const int rows = min(count, p.M - m0);
+  if constexpr (EPI == EPI_QKV_PAGED) {
+    // decode QKV: K and V features go straight into the batch rows' KV page slots
+    // (the lanes of a warp hold consecutive features: 64 contiguous bytes per row),
+    // Q features to C -- no separate kv_write pass
+    const int hd = p.kv.g.n_heads * p.kv.g.head_dim;
+    if (n >= hd) {
+      const int kv = n >= 2 * hd ? 1 : 0;
+      const int c = n - (1 + kv) * hd;
+      const int head = c / p.kv.g.head_dim, d = c % p.kv.g.head_dim;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j >= rows) break;
+        const TokenMeta m = p.kv.meta[m0 + j];
+        p.kv.pool[p.kv.g.offset(m.page, p.kv.layer, kv, head, m.slot) + d] =
+            __float2bfloat16(v[j] + b);
+      }
+      return;
+    }
+  }
   if constexpr (EPI == EPI_F32_BIAS_RESID) {
     // all residual loads first (independent), then the stores
     float* c = reinterpret_cast<float*>(p.C) + static_cast<size_t>(m0) * p.N + n;
@@ -1740,6 +1760,7 @@ static int skinny_epi(const CUtensorMap& tw, const CUtensorMap& tx, const GemmAr
     case EPI_BF16_BIAS_RELU: return launch_skinny<NB, EPI_BF16_BIAS_RELU>(tw, tx, a, ctas, s);
     case EPI_F32_BIAS_RESID: return launch_skinny<NB, EPI_F32_BIAS_RESID>(tw, tx, a, ctas, s);
     case EPI_F32: return launch_skinny<NB, EPI_F32>(tw, tx, a, ctas, s);
+    case EPI_QKV_PAGED: return launch_skinny<NB, EPI_QKV_PAGED>(tw, tx, a, ctas, s);
   }
   set_error("unknown gemm epilogue");
   return TK_EINVAL;
@@ -1931,7 +1952,7 @@ bool gemm_is_skinny(int M) { return M <= kSkinnyMaxM && !genv().no_skinny; }
 int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, int N, int K,
               int epi, void* workspace, int64_t ws_bytes, cudaStream_t stream, int max_ctas,
               const QkvScatter* scatter) {
-  TK_CHECK(epi != EPI_QKV_PAGED || (scatter && !gemm_is_skinny(M) && N % 32 == 0 &&
+  TK_CHECK(epi != EPI_QKV_PAGED || (scatter && N % 32 == 0 &&
                                     N == 3 * scatter->g.n_heads * scatter->g.head_dim &&
                                     scatter->g.head_dim % 32 == 0),
            TK_EINVAL, "gemm: EPI_QKV_PAGED needs a scatter target, M above the skinny range");
@@ -1984,6 +2005,7 @@ int gemm_bf16(const void* A, const void* B, void* C, const void* bias, int M, in
     rc = make_tmap_kmajor(&tx, A, M, K, pl.nb);
     if (rc) return rc;
     GemmArgs a{};
+    a.kv = scatter ? *scatter : QkvScatter{};
     a.C = C;
     a.bias = static_cast<const __nv_bfloat16*>(bias);
     a.M = M;
