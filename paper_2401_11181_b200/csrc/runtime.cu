@@ -454,10 +454,13 @@ static int run_layer(tk_instance* inst, int layer, int n, const TokenMeta* meta_
                            hi, m.norm_eps, !opt, s);
   });
   if (rc) return rc;
-  // OPT (no rotary embedding): the QKV epilogue writes K/V straight into the pages
-  // (chunk GEMMs and the decode skinny GEMMs alike); Llama: a kv_write pass (RoPE).
-  static const bool no_fused_decode_kv = getenv("TK_NO_FUSED_DECODE_KV") != nullptr;
-  const bool fused_kv = opt && !(no_fused_decode_kv && gemm_is_skinny(n));
+  // OPT (no rotary embedding) above the skinny range: the QKV epilogue writes K/V
+  // straight into the pages; otherwise a kv_write pass (RoPE for Llama).  The
+  // decode-size (skinny) GEMM can scatter K/V too (TK_FUSED_DECODE_KV=1), but its
+  // per-row 2-byte page stores made the QKV GEMM slower than the kv_write launch it
+  // saves (B=32: equal, B=128: -2%; profiles/r02_experiments.md).
+  static const bool fused_decode_kv = getenv("TK_FUSED_DECODE_KV") != nullptr;
+  const bool fused_kv = opt && (fused_decode_kv || !gemm_is_skinny(n));
   const QkvScatter scatter{meta_dev, inst->pool, inst->geom, layer};
   rc = profiled(inst, s, PK_QKV, 2 * nn * 3 * h * h, (3 * h * h + nn * 4 * h) * 2, [&] {
     return gemm_bf16(inst->xn, L.qkv_w, inst->qkv, L.qkv_b, n, 3 * hi, hi,
