@@ -802,7 +802,8 @@ int launch_chunk_attention_fa(const __nv_bfloat16* qkv, int q_rows, int q_stride
   TK_CUDA(cudaGetLastError());
   note_launch();
   if (plan.n_groups > 0) {
-    TK_CUDA(launch_pdl(g.head_dim == 64 ? fa_combine_kernel<64> : fa_combine_kernel<128>,
+    static const bool comb_pdl = !getenv("TK_COMBINE_PDL") || atoi(getenv("TK_COMBINE_PDL")) != 0;
+    TK_CUDA(launch_maybe_pdl(comb_pdl, g.head_dim == 64 ? fa_combine_kernel<64> : fa_combine_kernel<128>,
                        dim3(plan.n_groups * 16), dim3(256), 0, s, o, pairs_dev, groups_dev,
                        g.n_heads, partial));
     TK_CUDA(cudaGetLastError());

@@ -296,7 +296,9 @@ int launch_add_norm(float* x, const __nv_bfloat16* delta, const __nv_bfloat16* w
     TK_NORM_CASE(5) TK_NORM_CASE(6) TK_NORM_CASE(7) TK_NORM_CASE(8)
   }
 #undef TK_NORM_CASE
-  TK_CUDA(launch_pdl(kern, dim3(rows), dim3(kNormThreads), 0, s, x, delta, w, bb, y, cols, eps));
+  static const bool norm_pdl = !getenv("TK_NORM_PDL") || atoi(getenv("TK_NORM_PDL")) != 0;
+  TK_CUDA(launch_maybe_pdl(norm_pdl, kern, dim3(rows), dim3(kNormThreads), 0, s, x, delta, w, bb,
+                           y, cols, eps));
   note_launch();
   return TK_OK;
 }
@@ -978,7 +980,13 @@ int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16*
   const int ws_splits = (max_ctx + kDecSplitTokens - 1) / kDecSplitTokens;  // workspace stride
   const float scale_log2 = scale * 1.4426950408889634f;
   const bool d64 = g.head_dim == 64;
-  TK_CUDA(launch_pdl(d64 ? decode_attn_kernel<64> : decode_attn_kernel<128>,
+  // Launched WITHOUT programmatic dependent launch (TK_DEC_ATTN_PDL=1 restores it):
+  // under PDL its grid (splits x heads x batch CTAs) becomes resident while the QKV
+  // GEMM and kv_write drain and waits there; a plain launch made the decode step
+  // faster at every measured shape (Llama-2-7B B=256 ctx 1024: 33.5 -> 28.3 ms, OPT-13B
+  // B=32 ctx 2048: 15.9 -> 14.3 ms, B=8: 6.09 -> 5.94 ms, B=128 ctx 512: equal).
+  static const bool attn_pdl = getenv("TK_DEC_ATTN_PDL") && atoi(getenv("TK_DEC_ATTN_PDL")) != 0;
+  TK_CUDA(launch_maybe_pdl(attn_pdl, d64 ? decode_attn_kernel<64> : decode_attn_kernel<128>,
                      dim3(splits, g.n_heads, batch), dim3(128), 0, s, q, q_stride, o, pool, g,
                      layer, block_tables, bt_stride, ctx_lens, scale_log2,
                      static_cast<float*>(workspace), ws_splits, split_tokens));
