@@ -381,7 +381,10 @@ int launch_kv_write(__nv_bfloat16* qkv, const TokenMeta* meta, int n, __nv_bfloa
                     KvGeom g, int layer, float q_scale, int rope, float rope_theta,
                     cudaStream_t s) {
   if (n == 0) return TK_OK;
-  TK_CUDA(launch_pdl(kv_write_kernel, dim3(n), dim3(256), 0, s, qkv, meta, pool, g, layer, q_scale,
+  // plain launch by default (TK_KVW_PDL=1: PDL): decode step Llama-2-7B B=256 -2.1%,
+  // OPT-13B B=128 -0.6%, B=32 -0.2% (profiles/r02_experiments.md)
+  static const bool kvw_pdl = getenv("TK_KVW_PDL") && atoi(getenv("TK_KVW_PDL")) != 0;
+  TK_CUDA(launch_maybe_pdl(kvw_pdl, kv_write_kernel, dim3(n), dim3(256), 0, s, qkv, meta, pool, g, layer, q_scale,
                      rope, rope_theta));
   TK_CUDA(cudaGetLastError());
   note_launch();
@@ -992,7 +995,8 @@ int launch_decode_attention(const __nv_bfloat16* q, int q_stride, __nv_bfloat16*
                      static_cast<float*>(workspace), ws_splits, split_tokens));
   note_launch();
   if (splits > 1) {
-    TK_CUDA(launch_pdl(d64 ? decode_combine_kernel<64> : decode_combine_kernel<128>,
+    static const bool comb_pdl = !getenv("TK_DCOMB_PDL") || atoi(getenv("TK_DCOMB_PDL")) != 0;
+    TK_CUDA(launch_maybe_pdl(comb_pdl, d64 ? decode_combine_kernel<64> : decode_combine_kernel<128>,
                        dim3(g.n_heads, batch), dim3(128), 0, s, o, g.n_heads, ctx_lens,
                        static_cast<const float*>(workspace), ws_splits, split_tokens));
   note_launch();
