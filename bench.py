@@ -817,23 +817,14 @@ C3_MIX = {"LPLD": 0.5, "HPLD": 0.5}     # summarization-like (BASELINE configs[2
 C5_MIX = {"LPHD": 0.5, "HPHD": 0.5}     # content creation (BASELINE configs[4])
 
 
-def serving_leg(args, n_prefill: int, n_decode: int, n_requests: int, mixture: dict | None = None,
-                model: str | None = None, colocate: bool = False, coupled: bool = False,
-                streaming: bool = False, capacity_tokens: int | None = None) -> dict:
-    """One serving run through the reference scheduler + CUDA executor (real
-    clock, completion stamps = CUDA-event times) on GPUs 0.. (p{i} then d{j}),
-    or every instance on GPU 0 when ``colocate``, beside the same workload on the modeled clock (pdsim's V100 cost
-    model through this package's bit-identical port; its single-thread wall time
-    is the CPU baseline of the scheduler, BASELINE.md section 4)."""
-    import paper_2401_11181_b200 as tk
+def serving_config(seed: int, n_prefill: int, n_decode: int, n_requests: int,
+                   mixture: dict | None = None, model: str = "opt-13b", colocate: bool = False,
+                   coupled: bool = False, capacity_tokens: int | None = None) -> dict:
+    """The experiment config of one serving leg (pdsim keys + devices / model):
+    p{i} on GPU i, d{j} on GPU n_prefill + j, or all on GPU 0 when ``colocate``.
+    Device-free, so the CPU tests check every leg's config and scheduling."""
     from paper_2401_11181_b200 import native
-    from paper_2401_11181_b200.experiment import run_experiment
-    model = model or args.model
     shape = native.MODELS[model]
-    n_gpus = 1 if colocate else n_prefill + n_decode
-    if n_gpus > native.device_count():
-        raise RuntimeError(f"{n_prefill}P:{n_decode}D needs {n_gpus} GPUs, "
-                           f"{native.device_count()} visible")
     wl = {"n_requests": n_requests}
     if mixture:
         wl["mixture"] = dict(mixture)
@@ -841,7 +832,7 @@ def serving_leg(args, n_prefill: int, n_decode: int, n_requests: int, mixture: d
     if capacity_tokens:
         cm["mem_capacity_tokens"] = capacity_tokens
     mcfg = {"name": model, "prefill_pages": 2048, "staging_pages": 512,
-            "max_decode_batch": 256, "seed": args.seed}
+            "max_decode_batch": 256, "seed": seed}
     if capacity_tokens is None:
         mcfg["capacity_from_hbm"] = True
     devices = {}
@@ -858,10 +849,34 @@ def serving_leg(args, n_prefill: int, n_decode: int, n_requests: int, mixture: d
            "devices": devices}
     if coupled:
         cfg["system"] = "coupled"
+    return cfg
+
+
+def sim_config(cfg: dict) -> dict:
+    """The same leg on pdsim's modeled clock (no device keys the sim rejects)."""
+    return dict(cfg, model={k: v for k, v in cfg["model"].items() if k != "capacity_from_hbm"})
+
+
+def serving_leg(args, n_prefill: int, n_decode: int, n_requests: int, mixture: dict | None = None,
+                model: str | None = None, colocate: bool = False, coupled: bool = False,
+                streaming: bool = False, capacity_tokens: int | None = None) -> dict:
+    """One serving run through the reference scheduler + CUDA executor (real
+    clock, completion stamps = CUDA-event times) on GPUs 0.. (p{i} then d{j}),
+    or every instance on GPU 0 when ``colocate``, beside the same workload on the modeled clock (pdsim's V100 cost
+    model through this package's bit-identical port; its single-thread wall time
+    is the CPU baseline of the scheduler, BASELINE.md section 4)."""
+    import paper_2401_11181_b200 as tk
+    from paper_2401_11181_b200 import native
+    from paper_2401_11181_b200.experiment import run_experiment
+    model = model or args.model
+    n_gpus = 1 if colocate else n_prefill + n_decode
+    if n_gpus > native.device_count():
+        raise RuntimeError(f"{n_prefill}P:{n_decode}D needs {n_gpus} GPUs, "
+                           f"{native.device_count()} visible")
+    cfg = serving_config(args.seed, n_prefill, n_decode, n_requests, mixture, model, colocate,
+                         coupled, capacity_tokens)
     t0 = time.perf_counter()
-    sim = run_experiment(tk.config_from_dict(dict(cfg, model={k: v for k, v in mcfg.items()
-                                                               if k != "capacity_from_hbm"})),
-                         seed=args.seed).summary
+    sim = run_experiment(tk.config_from_dict(sim_config(cfg)), seed=args.seed).summary
     sim_wall = time.perf_counter() - t0
     dev_cfg = dict(cfg, executor="cuda")
     if streaming:
@@ -919,6 +934,16 @@ def serving_run(args) -> dict:
     return out
 
 
+# P:D-split serving legs per GPU count (BASELINE.json configs[2..4]):
+# (name, prefill instances, decode instances, mixture, model)
+MULTI_GPU_LEGS = {
+    2: [("c3_1p1d", 1, 1, C3_MIX, None)],
+    4: [("c4_1p3d", 1, 3, None, None), ("c4_2p2d", 2, 2, None, None)],
+    8: [("c4_2p6d", 2, 6, None, None), ("c4_4p4d", 4, 4, None, None),
+        ("c5_llama_2p6d", 2, 6, C5_MIX, "llama-2-7b")],
+}
+
+
 def multi_gpu_run(args, n: int, peaks: dict) -> dict:
     """The disaggregated system on n GPUs of this box (one host process drives
     every instance; pdsim/control.py's scheduler is centralised):
@@ -933,12 +958,8 @@ def multi_gpu_run(args, n: int, peaks: dict) -> dict:
     gbs = p2p if isinstance(p2p, float) else None
     out["kv_handoff_nvlink"] = guarded(lambda: handoff_run(args, shape, 0, 1, peaks, p2p_gbs=gbs))
     out["overlap_nvlink"] = guarded(lambda: overlap_run(args, shape, 0, 1))
-    legs = {2: [("c3_1p1d", 1, 1, C3_MIX, None)],
-            4: [("c4_1p3d", 1, 3, None, None), ("c4_2p2d", 2, 2, None, None)],
-            8: [("c4_2p6d", 2, 6, None, None), ("c4_4p4d", 4, 4, None, None),
-                ("c5_llama_2p6d", 2, 6, C5_MIX, "llama-2-7b")]}
     n_req = {"c5_llama_2p6d": args.c5_n}
-    for name, p, d, mix, model in legs.get(n, []):
+    for name, p, d, mix, model in MULTI_GPU_LEGS.get(n, []):
         out[name] = guarded(lambda: serving_leg(args, p, d, n_req.get(name, args.serving_multi_n),
                                                 mixture=mix, model=model))
     return out
