@@ -41,6 +41,11 @@ pytestmark = pytest.mark.gpu
 
 GOLDEN = Path(__file__).parent / "golden" / "sched_decisions.json.gz"
 MODEL = native.TINY_LONG
+# OPT-13B width (2 layers) with the 10,240-row position table: the replay then runs the
+# benchmarked kernels -- M=512 pair / 144-wide GEMM schedules, the QKV->page epilogue at
+# 40 heads, attention pieces over real prefixes, graph decode steps at many buckets
+OPT13B_2L = native.ModelShape("opt13b-2l", native.TK_ARCH_OPT, 2, 5120, 40, 20480, 50272,
+                              max_positions=10240)
 SEED = 0
 
 
@@ -49,16 +54,15 @@ def _golden(name):
         return json.loads(fh.read())[name]
 
 
-def _oracle():
-    inst = native.Instance(MODEL, device=0, seed=SEED, kv_pages=8, page_tokens=16, max_chunk=16)
-    m = MODEL
+def _oracle(m=MODEL):
+    inst = native.Instance(m, device=0, seed=SEED, kv_pages=8, page_tokens=16, max_chunk=16)
     ora = OracleModel.from_instance(Shape(m.arch, m.n_layers, m.hidden, m.n_heads, m.ffn,
                                           m.vocab, m.max_positions), inst, device="cuda")
     inst.close()
     return ora
 
 
-def _check_tokens(ora, requests, token_log, picks):
+def _check_tokens(ora, requests, token_log, picks, model=MODEL):
     """Teacher-forced oracle over prompt + generated tokens of the picked requests."""
     decided = total = 0
     for rid in picks:
@@ -66,7 +70,7 @@ def _check_tokens(ora, requests, token_log, picks):
         gen = token_log[rid]
         # first token + one per decode step (pdsim/decode.py:336-351)
         assert len(gen) == req.true_decode_len + 1, (rid, len(gen), req.true_decode_len)
-        prompt = token_ids_for(req, MODEL.vocab, SEED)
+        prompt = token_ids_for(req, model.vocab, SEED)
         seq = prompt + gen[:-1]
         ref = ora.full_forward(seq)[len(prompt) - 1:].float().cpu()
         g = torch.tensor(gen, dtype=torch.long)
@@ -82,11 +86,16 @@ def _check_tokens(ora, requests, token_log, picks):
     return decided, total
 
 
-@pytest.mark.parametrize("name,n_check", [("c1_mixed128_1p1d_roce", 16), ("greedy_swaps", 10),
-                                          ("coupled_64", 10)])
-def test_replay_reproduces_reference_decisions_and_oracle_tokens(name, n_check):
+@pytest.mark.parametrize("name,n_check,model", [("c1_mixed128_1p1d_roce", 16, MODEL),
+                                                ("greedy_swaps", 10, MODEL),
+                                                ("coupled_64", 10, MODEL),
+                                                ("c1_mixed128_1p1d_roce", 8, OPT13B_2L)],
+                         ids=["mixed128-tiny", "greedy_swaps-tiny", "coupled64-tiny",
+                              "mixed128-opt13b-width"])
+def test_replay_reproduces_reference_decisions_and_oracle_tokens(name, n_check, model):
     case = _golden(name)
-    cfg = dict(case["config"], executor="replay", model={"name": MODEL.name, "seed": SEED,
+    native.MODELS.setdefault(model.name, model)
+    cfg = dict(case["config"], executor="replay", model={"name": model.name, "seed": SEED,
                                                                "prefill_pages": 8192})
     res = tk.run_experiment(tk.config_from_dict(cfg), seed=case["seed"])
     got = json.loads(json.dumps(_trace(res)))
@@ -102,14 +111,17 @@ def test_replay_reproduces_reference_decisions_and_oracle_tokens(name, n_check):
     ex_log = res.control.executor.token_log
     requests = {rid: rec.req for rid, rec in res.control.table.items()}
     assert set(ex_log) == set(requests), "every request generated tokens on the device"
-    # sample: the longest prompts, the longest decodes, and an even spread of ids
-    by_prompt = sorted(requests, key=lambda r: -requests[r].prompt_len)[:3]
-    by_decode = sorted(requests, key=lambda r: -requests[r].true_decode_len)[:3]
-    ids = sorted(requests)
+    # sample: the longest prompts, the longest decodes, and an even spread of ids (at
+    # OPT-13B width, sequences up to 4k tokens: the oracle's dense [H, n, n] scores)
+    cap = 4096 if model.hidden > 1024 else 1 << 30
+    cand = {r: q for r, q in requests.items() if q.prompt_len + q.true_decode_len <= cap}
+    by_prompt = sorted(cand, key=lambda r: -cand[r].prompt_len)[:3]
+    by_decode = sorted(cand, key=lambda r: -cand[r].true_decode_len)[:3]
+    ids = sorted(cand)
     spread = [ids[int(i * len(ids) / (n_check - 6))] for i in range(n_check - 6)]
     picks = list(dict.fromkeys(by_prompt + by_decode + spread))
-    ora = _oracle()
-    decided, total = _check_tokens(ora, requests, ex_log, picks)
-    record(f"replay_{name}", requests_checked=len(picks), tokens=total, decided=decided,
-           chunks=n_chunks, iterations=n_iters)
+    ora = _oracle(model)
+    decided, total = _check_tokens(ora, requests, ex_log, picks, model)
+    record(f"replay_{name}_{model.name}", requests_checked=len(picks), tokens=total,
+           decided=decided, chunks=n_chunks, iterations=n_iters)
     assert decided >= total // 3, (decided, total)
