@@ -121,7 +121,10 @@ int tk_prefill_chunk(tk_instance* inst, int32_t n_tokens, const int32_t* token_i
 /* One continuous-batching decode iteration over B rows (pdsim running order).
  * Row b: input token last_tokens[b] at position ctx_lens[b] (tokens already in
  * KV); its K/V is appended into page block_tables[b*bt_stride + ctx/pt].
- * next_tokens_out[b] receives the greedy next token.                         */
+ * next_tokens_out[b] receives the greedy next token.  Without logits_out the
+ * step runs as a CUDA graph recorded once per (batch bucket, 1024-token context
+ * bucket) of the instance (TK_NO_DECODE_GRAPH=1: eager launches); the result is
+ * the same computation.                                                        */
 int tk_decode_step(tk_instance* inst, int32_t batch, const int32_t* last_tokens,
                    const int32_t* ctx_lens, const int32_t* block_tables, int32_t bt_stride,
                    int32_t* next_tokens_out, float* logits_out, tk_event** ev);
