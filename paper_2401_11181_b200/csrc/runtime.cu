@@ -460,7 +460,8 @@ static int run_layer(tk_instance* inst, int layer, int n, const TokenMeta* meta_
   // per-row 2-byte page stores made the QKV GEMM slower than the kv_write launch it
   // saves (B=32: equal, B=128: -2%; profiles/r02_experiments.md).
   static const bool fused_decode_kv = getenv("TK_FUSED_DECODE_KV") != nullptr;
-  const bool fused_kv = opt && (fused_decode_kv || !gemm_is_skinny(n));
+  static const bool no_fused_kv = getenv("TK_NO_FUSED_KV") != nullptr;  // experiments
+  const bool fused_kv = opt && !no_fused_kv && (fused_decode_kv || !gemm_is_skinny(n));
   const QkvScatter scatter{meta_dev, inst->pool, inst->geom, layer};
   rc = profiled(inst, s, PK_QKV, 2 * nn * 3 * h * h, (3 * h * h + nn * 4 * h) * 2, [&] {
     return gemm_bf16(inst->xn, L.qkv_w, inst->qkv, L.qkv_b, n, 3 * hi, hi,
