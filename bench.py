@@ -254,6 +254,15 @@ def barrier(world: int):
         dist.barrier()
 
 
+def leave_group(world: int):
+    """Tear the process group down once the last collective is done (torchrun ranks
+    exit while rank 0 alone runs the multi-GPU legs)."""
+    if world > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -388,6 +397,7 @@ def run_ours(args, world, rank, local):
     if rank != 0:
         inst.close()
         barrier(world)  # rank 0 runs the cross-GPU legs once every replica is closed
+        leave_group(world)
         return
     line = {
         "metric": METRIC,
@@ -437,6 +447,7 @@ def run_ours(args, world, rank, local):
     inst.close()
     if n_gpus > 1:
         barrier(world)  # every other rank has closed its replica
+        leave_group(world)  # no collective is pending while the single-process legs run
         line["multi_gpu"] = guarded(lambda: multi_gpu_run(args, n_gpus, peaks))
     if n_gpus == 1 and not args.no_decode:
         line["decode"] = decode_run(args, shape, local, peaks)
@@ -989,9 +1000,7 @@ def main():
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    leave_group(world)
 
 
 if __name__ == "__main__":

@@ -42,8 +42,12 @@ def _worker(rank, world, port, q):
     w, r, local = bench.dist_setup("gloo")
     bench.barrier(w)
     got = bench.dist_max(float(r + 1) * 1.5, w)   # per-rank "device seconds"
-    q.put((r, w, local, got))
-    dist.destroy_process_group()
+    bench.barrier(w)
+    # the bench's hand-off: every rank leaves the group after the last collective,
+    # then rank 0 alone runs the single-process multi-GPU legs; leaving twice is safe
+    bench.leave_group(w)
+    bench.leave_group(w)
+    q.put((r, w, local, got, dist.is_initialized()))
 
 
 def test_bench_max_over_ranks_gloo():
@@ -56,7 +60,7 @@ def test_bench_max_over_ranks_gloo():
     res = sorted(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res == [(0, 2, 0, 3.0), (1, 2, 1, 3.0)]
+    assert res == [(0, 2, 0, 3.0, False), (1, 2, 1, 3.0, False)]
 
 
 def test_reference_arm_other_ranks_exit_quietly(capsys):
