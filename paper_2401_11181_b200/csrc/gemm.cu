@@ -17,11 +17,12 @@
 // persistent CTAs (stream-K).  A tile owned by one CTA is written directly;
 // a tile shared by several CTAs is reduced without atomics on the data: each
 // contributor takes an arrival number from a per-tile counter; every arrival
-// but the last stores its fp32 partial into its own slot of the workspace
-// (thread-major, 512 contiguous bytes per warp access) and raises its
-// ready flag with a release store; the last arrival acquires the earlier
-// flags, adds their partials to its TMEM accumulator, runs the epilogue and
-// re-zeroes the counter and flags.  The last arrival only ever waits on CTAs
+// but the last stores its fp32 partial into the slot of its contributor rank
+// (k order; thread-major, 512 contiguous bytes per warp access) and raises that
+// rank's ready flag with a release store; the last arrival acquires the other
+// flags, sums the partials in rank order with its own TMEM accumulator at its
+// rank (so the result is bit-identical whatever the arrival order), runs the
+// epilogue and re-zeroes the counter and flags.  The last arrival only ever waits on CTAs
 // that already hold an arrival number (i.e. are running and past their MMAs),
 // so the scheme is deadlock-free at any occupancy, including when another
 // instance's kernels share the GPU.  This fixes the
@@ -270,6 +271,30 @@ __device__ __forceinline__ void partial_load(const float* tile_ws, size_t slot_e
     for (int g = 0; g < 8; ++g) {
       const float4 t = __ldcg(src + g * 128);
       out[g].x += t.x; out[g].y += t.y; out[g].z += t.z; out[g].w += t.w;
+    }
+  }
+}
+
+// Split tiles with 3+ contributors: chunk c summed in contributor (k) order, the
+// finishing CTA's own accumulator at its own rank, so the result does not depend on
+// which contributor arrives last (with 2, a + b == b + a already makes it exact).
+__device__ __forceinline__ void ranked_sum(const float* tile_ws, size_t slot_elems, int contrib,
+                                           int me, int c, int tid, const uint32_t (&own)[32],
+                                           float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = 0.f;
+  for (int a = 0; a < contrib; ++a) {
+    if (a == me) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(own[j]);
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(tile_ws + a * slot_elems) +
+                          static_cast<size_t>(c) * 8 * 128 + tid;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const float4 t = __ldcg(src + g * 128);
+        v[g * 4] += t.x; v[g * 4 + 1] += t.y; v[g * 4 + 2] += t.z; v[g * 4 + 3] += t.w;
+      }
     }
   }
 }
@@ -533,8 +558,10 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
         const size_t slot_elems = static_cast<size_t>(BN / 32) * 128 * 32;
         float* tile_ws = p.ws + static_cast<size_t>(tile) * p.slots * slot_elems;
         const int tid_e = static_cast<int>(threadIdx.x) - 64;  // 0..127, epilogue thread index
+        // slots are indexed by contributor rank (k order), not arrival
+        const int me = cluster - owner_of(tile_first, T, G);
         if (arrival < contrib - 1) {
-          float* mine = tile_ws + static_cast<size_t>(arrival) * slot_elems;
+          float* mine = tile_ws + static_cast<size_t>(me) * slot_elems;
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             uint32_t r[32];
@@ -547,23 +574,36 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
           if (lane == 0) mbar_arrive(&tempty[acc]);
           __threadfence();
           named_bar_sync(1, 128);
-          if (leader) st_release(flags + arrival, 1);
+          if (leader) st_release(flags + me, 1);
         } else {
           if (leader) {
-            for (int a = 0; a < contrib - 1; ++a)
-              while (ld_acquire(flags + a) == 0) {
+            for (int a = 0; a < contrib; ++a)
+              while (a != me && ld_acquire(flags + a) == 0) {
               }
           }
           named_bar_sync(1, 128);
           __threadfence();
-          fixup_epilogue<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems, contrib - 1,
-                                       tid_e);
+          if (contrib == 2) {
+            fixup_epilogue<EPI, BN / 32>(p, t_row, row, col_base,
+                                         tile_ws + static_cast<size_t>(1 - me) * slot_elems,
+                                         slot_elems, 1, tid_e);
+          } else {
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(t_row + c * 32, r);
+              tmem_wait_ld();
+              float v[32];
+              ranked_sum(tile_ws, slot_elems, contrib, me, c, tid_e, r, v);
+              epilogue_store<EPI>(p, row, col_base + c * 32, v);
+            }
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
           named_bar_sync(1, 128);
           if (leader) {
-            for (int a = 0; a < contrib - 1; ++a) flags[a] = 0;
+            for (int a = 0; a < contrib; ++a) flags[a] = 0;
             *counter = 0;
           }
         }
@@ -825,8 +865,12 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
         const int arrival = *last_flag;
         const size_t slot_elems = static_cast<size_t>(NB) * 128;
         float* tile_ws = p.ws + static_cast<size_t>(tile) * p.slots * slot_elems;
+        // slots indexed by contributor rank (k order): the finishing CTA sums in that
+        // order with its own accumulator at its rank -- arrival order cannot change
+        // the rounding
+        const int me = static_cast<int>(blockIdx.x) - owner_of(tile_first, T, G);
         if (arrival < contrib - 1) {
-          float* mine = tile_ws + static_cast<size_t>(arrival) * slot_elems;
+          float* mine = tile_ws + static_cast<size_t>(me) * slot_elems;
 #pragma unroll 1
           for (int c = 0; c < NB / CH; ++c) {
             uint32_t r[32];
@@ -844,11 +888,11 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
           if (lane == 0) mbar_arrive(&tempty[acc]);
           __threadfence();
           named_bar_sync(1, 128);
-          if (leader) st_release(flags + arrival, 1);
+          if (leader) st_release(flags + me, 1);
         } else {
           if (leader) {
-            for (int a = 0; a < contrib - 1; ++a)
-              while (ld_acquire(flags + a) == 0) {
+            for (int a = 0; a < contrib; ++a)
+              while (a != me && ld_acquire(flags + a) == 0) {
               }
           }
           named_bar_sync(1, 128);
@@ -861,8 +905,13 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
             tmem_wait_ld();
             float v[32];
 #pragma unroll
-            for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(r[j]);
-            for (int a = 0; a < contrib - 1; ++a) {
+            for (int j = 0; j < CH; ++j) v[j] = 0.f;
+            for (int a = 0; a < contrib; ++a) {
+              if (a == me) {
+#pragma unroll
+                for (int j = 0; j < CH; ++j) v[j] += __uint_as_float(r[j]);
+                continue;
+              }
               const float4* src = reinterpret_cast<const float4*>(
                   tile_ws + static_cast<size_t>(a) * slot_elems + (static_cast<size_t>(c) * 128 + tid_e) * CH);
 #pragma unroll
@@ -878,7 +927,7 @@ __global__ void __launch_bounds__(SkinnyCfg<NB>::THREADS, 1)
           if (lane == 0) mbar_arrive(&tempty[acc]);
           named_bar_sync(1, 128);
           if (leader) {
-            for (int a = 0; a < contrib - 1; ++a) flags[a] = 0;
+            for (int a = 0; a < contrib; ++a) flags[a] = 0;
             *counter = 0;
           }
         }
@@ -1306,8 +1355,11 @@ __global__ void __launch_bounds__(192, 1)
         const int arrival = *last_flag;
         const size_t slot_elems = static_cast<size_t>(BN / 32) * 128 * 32;
         float* tile_ws = p.ws + static_cast<size_t>(tile) * p.slots * slot_elems;
+        // slots are indexed by contributor rank (k order), not arrival: the finishing
+        // CTA's sum does not depend on which contributor arrives last
+        const int me = cluster - owner_of(tile_first, T, G);
         if (arrival < contrib - 1) {
-          float* mine = tile_ws + static_cast<size_t>(arrival) * slot_elems;
+          float* mine = tile_ws + static_cast<size_t>(me) * slot_elems;
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             uint32_t r[32];
@@ -1318,81 +1370,96 @@ __global__ void __launch_bounds__(192, 1)
           release_tmem();
           __threadfence();
           named_bar_sync(1, 128);
-          if (ep_leader) st_release(flags + arrival, 1);
+          if (ep_leader) st_release(flags + me, 1);
         } else {
           if (ep_leader) {
-            for (int a = 0; a < contrib - 1; ++a)
-              while (ld_acquire(flags + a) == 0) {
+            for (int a = 0; a < contrib; ++a)
+              while (a != me && ld_acquire(flags + a) == 0) {
               }
             if (seg_end == it_end) gemm_cta_stamp(p, 6);
           }
           named_bar_sync(1, 128);
           __threadfence();
-          // Final fixup of the CTA: one bulk copy brings every partial slot into the
-          // idle ring behind the staging tile (one round trip instead of one per
-          // 32-column chunk, which left ~7 us on the critical path).
-          const int nsl = contrib - 1;
-          constexpr int kStageArea = (128 * ROWB + 1023) & ~1023;
-          const bool bulk = staged && kStageArea + nsl * static_cast<int>(slot_elems) * 4 <=
-                                          STAGES * STAGE_BYTES;
-          if (bulk) {
-            float* pbuf = reinterpret_cast<float*>(smem + kStageArea);
-            if (ep_leader) {
-              fence_proxy_async_global();
-              const uint32_t slot_bytes = static_cast<uint32_t>(slot_elems) * 4;
-              mbar_expect_tx(fix_bar, nsl * slot_bytes);
-              for (int a = 0; a < nsl; ++a)
+          if (contrib == 2) {
+            // one other partial: own + other is exact in either order
+            const float* ows = tile_ws + static_cast<size_t>(1 - me) * slot_elems;
+            // Final fixup of the CTA: one bulk copy brings the partial into the idle
+            // ring behind the staging tile (one round trip instead of one per 32-column
+            // chunk, which left ~7 us on the critical path).
+            constexpr int kStageArea = (128 * ROWB + 1023) & ~1023;
+            const bool bulk = staged && kStageArea + static_cast<int>(slot_elems) * 4 <=
+                                            STAGES * STAGE_BYTES;
+            if (bulk) {
+              float* pbuf = reinterpret_cast<float*>(smem + kStageArea);
+              if (ep_leader) {
+                fence_proxy_async_global();
+                const uint32_t slot_bytes = static_cast<uint32_t>(slot_elems) * 4;
+                mbar_expect_tx(fix_bar, slot_bytes);
                 for (uint32_t off = 0; off < slot_bytes; off += 32768)
-                  bulk_g2s(reinterpret_cast<uint8_t*>(pbuf + a * slot_elems) + off,
-                           reinterpret_cast<const uint8_t*>(tile_ws + a * slot_elems) + off,
+                  bulk_g2s(reinterpret_cast<uint8_t*>(pbuf) + off,
+                           reinterpret_cast<const uint8_t*>(ows) + off,
                            slot_bytes - off < 32768 ? slot_bytes - off : 32768, fix_bar);
-            }
-            mbar_wait(fix_bar, 0);
-            const float4* p4 = reinterpret_cast<const float4*>(pbuf);
-            stage_and_store([&](int c, float (&v)[32]) {
-              uint32_t r[32];
-              tmem_ld_32x32b_x32(t_row + c * 32, r);
-              tmem_wait_ld();
-#pragma unroll
-              for (int g = 0; g < 8; ++g) {
-                float4 q = p4[(c * 8 + g) * 128 + tid_e];
-                for (int a = 1; a < nsl; ++a) {
-                  const float4 t = p4[a * (slot_elems / 4) + (c * 8 + g) * 128 + tid_e];
-                  q.x += t.x; q.y += t.y; q.z += t.z; q.w += t.w;
-                }
-                v[g * 4] = __uint_as_float(r[g * 4]) + q.x;
-                v[g * 4 + 1] = __uint_as_float(r[g * 4 + 1]) + q.y;
-                v[g * 4 + 2] = __uint_as_float(r[g * 4 + 2]) + q.z;
-                v[g * 4 + 3] = __uint_as_float(r[g * 4 + 3]) + q.w;
               }
-            });
+              mbar_wait(fix_bar, 0);
+              const float4* p4 = reinterpret_cast<const float4*>(pbuf);
+              stage_and_store([&](int c, float (&v)[32]) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(t_row + c * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                  const float4 q = p4[(c * 8 + g) * 128 + tid_e];
+                  v[g * 4] = __uint_as_float(r[g * 4]) + q.x;
+                  v[g * 4 + 1] = __uint_as_float(r[g * 4 + 1]) + q.y;
+                  v[g * 4 + 2] = __uint_as_float(r[g * 4 + 2]) + q.z;
+                  v[g * 4 + 3] = __uint_as_float(r[g * 4 + 3]) + q.w;
+                }
+              });
+            } else if (staged) {
+              stage_and_store([&](int c, float (&v)[32]) {
+                float4 q[8];
+                partial_load(ows, slot_elems, 1, c, tid_e, q);
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(t_row + c * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                  v[g * 4] = __uint_as_float(r[g * 4]) + q[g].x;
+                  v[g * 4 + 1] = __uint_as_float(r[g * 4 + 1]) + q[g].y;
+                  v[g * 4 + 2] = __uint_as_float(r[g * 4 + 2]) + q[g].z;
+                  v[g * 4 + 3] = __uint_as_float(r[g * 4 + 3]) + q[g].w;
+                }
+              });
+            } else {
+              if (kGemmExp && p.fix_depth >= 2)
+                fixup_epilogue_deep<EPI, BN / 32>(p, t_row, row, col_base, ows, slot_elems, 1,
+                                                  tid_e);
+              else
+                fixup_epilogue<EPI, BN / 32>(p, t_row, row, col_base, ows, slot_elems, 1, tid_e);
+              release_tmem();
+            }
           } else if (staged) {
             stage_and_store([&](int c, float (&v)[32]) {
-              float4 q[8];
-              partial_load(tile_ws, slot_elems, contrib - 1, c, tid_e, q);
               uint32_t r[32];
               tmem_ld_32x32b_x32(t_row + c * 32, r);
               tmem_wait_ld();
-#pragma unroll
-              for (int g = 0; g < 8; ++g) {
-                v[g * 4] = __uint_as_float(r[g * 4]) + q[g].x;
-                v[g * 4 + 1] = __uint_as_float(r[g * 4 + 1]) + q[g].y;
-                v[g * 4 + 2] = __uint_as_float(r[g * 4 + 2]) + q[g].z;
-                v[g * 4 + 3] = __uint_as_float(r[g * 4 + 3]) + q[g].w;
-              }
+              ranked_sum(tile_ws, slot_elems, contrib, me, c, tid_e, r, v);
             });
           } else {
-            if (kGemmExp && p.fix_depth >= 2)
-              fixup_epilogue_deep<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems,
-                                                contrib - 1, tid_e);
-            else
-              fixup_epilogue<EPI, BN / 32>(p, t_row, row, col_base, tile_ws, slot_elems,
-                                           contrib - 1, tid_e);
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(t_row + c * 32, r);
+              tmem_wait_ld();
+              float v[32];
+              ranked_sum(tile_ws, slot_elems, contrib, me, c, tid_e, r, v);
+              epilogue_store<EPI>(p, row, col_base + c * 32, v);
+            }
             release_tmem();
           }
           named_bar_sync(1, 128);
           if (ep_leader) {
-            for (int a = 0; a < contrib - 1; ++a) flags[a] = 0;
+            for (int a = 0; a < contrib; ++a) flags[a] = 0;
             *counter = 0;
           }
         }
@@ -1621,7 +1688,7 @@ static GemmPlan plan_skinny(int M, int N, int K, int max_ctas) {
                   owner_of(t * pl.kbs, pl.total_iters, ctas) + 1;
     most = std::max(most, c);
   }
-  pl.slots = most - 1;
+  pl.slots = most;  // rank-indexed partial slots (the finishing rank leaves its own unused)
   pl.ws_bytes = kCounterBytes + static_cast<int64_t>(pl.tiles_n) * pl.slots * 128LL * pl.nb * 4;
   pl.counters_fit = static_cast<int64_t>(pl.tiles_n) * (1 + pl.slots) * 4 <= kCounterBytes;
   return pl;
@@ -1709,7 +1776,7 @@ static GemmPlan plan_gemm(int M, int N, int K, int max_ctas) {
                   owner_of(t * pl.kbs, pl.total_iters, clusters) + 1;
     most = std::max(most, c);
   }
-  pl.slots = most - 1;
+  pl.slots = most;  // rank-indexed partial slots (the finishing rank leaves its own unused)
   const int64_t tiles = static_cast<int64_t>(pl.tiles_m) * pl.tiles_n;
   // [kCounterBytes: per-tile counters + ready flags, always left zeroed][partial slots]
   pl.ws_bytes = kCounterBytes + tiles * pl.slots * 128LL * pl.bn * 4;

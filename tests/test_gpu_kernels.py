@@ -310,3 +310,26 @@ def test_gemm_shared_workspace_across_shapes():
             out = native.gemm(a, b, epilogue=native.EPI_F32, workspace=ws)
             torch.cuda.synchronize()
             assert _rel_err(out, a.float() @ b.float().t()) < 2e-3, (M, N, K)
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (512, 2560, 20480),  # pair kernel, 3-4 contributors per split tile
+    (16, 5120, 20480),   # skinny (decode) GEMM, up to 16 contributors per tile
+    (100, 20480, 5120),  # skinny NB=128
+    (384, 5120, 20480),  # odd m-tile count: the 1-CTA kernel's fixup
+])
+def test_gemm_is_deterministic(M, N, K):
+    """Split (stream-K) tiles are summed in contributor order with the finishing
+    CTA's own accumulator at its rank, so repeated runs are bit-identical whatever
+    the arrival order of the contributors."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    outs = []
+    for _ in range(6):
+        outs.append(native.gemm(a, b, epilogue=native.EPI_F32).clone())
+        torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    ref = a.float() @ b.float().t()
+    assert _rel_err(outs[0], ref) < 2e-3
