@@ -258,3 +258,41 @@ def test_decode_graph_steps_match_eager(model):
         last = [int(t) for t in e_toks]
     assert checked >= 15
     inst.close()
+
+
+def test_runs_are_bit_reproducible():
+    """Same weights, same inputs, two fresh instances: prefill logits, KV pages and
+    decode logits are bitwise identical (split GEMM tiles and attention pieces are
+    reduced in a fixed order, never in arrival order)."""
+    model = native.ModelShape("opt-2l-1k", native.TK_ARCH_OPT, 2, 1024, 8, 4096, 8192,
+                              max_positions=2048)
+    lens = [18, 100, 512, 900]
+    runs = []
+    for _ in range(2):
+        reqs, tables, n_pages, chunks = _plan(lens, 512)
+        inst = native.Instance(model, device=0, seed=4, kv_pages=n_pages, page_tokens=PT,
+                               max_chunk=512)
+        prompts = {r.id: token_ids_for(r, model.vocab, seed=5) for r in reqs}
+        out = []
+        for chunk in chunks:
+            ids, slices, bt = [], [], []
+            for rid, start, n in chunk.slices:
+                ids += prompts[rid][start:start + n]
+                slices.append((start, n, len(bt), len(tables[rid]), int(start + n == lens[rid])))
+                bt += tables[rid]
+            ev, toks, logits = inst.prefill_chunk(ids, slices, bt, want_logits=True)
+            ev.wait()
+            out.append(logits.copy())
+        stride = max(len(t) for t in tables.values())
+        bt = sum((tables[i] + [0] * (stride - len(tables[i])) for i in range(len(lens))), [])
+        last = [3, 4, 5, 6]
+        for step in range(3):
+            ev, toks = inst.decode_step(last, [n + step for n in lens], bt, stride)
+            ev.wait()
+            last = [int(t) for t in toks]
+            out.append(np.array(last))
+        out.append(np.stack([inst.read_page(p) for p in range(n_pages)]))
+        inst.close()
+        runs.append(out)
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)
