@@ -1679,6 +1679,16 @@ static GemmPlan plan_skinny(int M, int N, int K, int max_ctas) {
   // than all SMs): the next GEMM's CTAs start on the free SMs and stream their first
   // weight tiles (PDL) while this one drains.  TK_GEMM_SKINNY_CTAS overrides.
   int ctas = std::min(max_skinny_ctas(pl.nb), genv().skinny_ctas > 0 ? genv().skinny_ctas : 120);
+  // TK_GEMM_SKINNY_MAP="N,K,G;...": per-shape CTA counts (experiments)
+  if (const char* m = getenv("TK_GEMM_SKINNY_MAP")) {
+    int n_, k_, g_, used = 0;
+    while (sscanf(m, "%d,%d,%d%n", &n_, &k_, &g_, &used) == 3) {
+      if (n_ == N && k_ == K) ctas = std::min(max_skinny_ctas(pl.nb), g_);
+      m += used;
+      if (*m != ';') break;
+      ++m;
+    }
+  }
   if (max_ctas > 0) ctas = std::min(ctas, max_ctas);
   ctas = static_cast<int>(std::min<long long>(ctas, std::max<long long>(1, pl.total_iters / 4)));
   pl.clusters = ctas;
