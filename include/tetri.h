@@ -134,7 +134,8 @@ int tk_decode_step(tk_instance* inst, int32_t batch, const int32_t* last_tokens,
 int tk_kv_send(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
                const int32_t* dst_pages, int32_t n_pages, tk_event** ev);
 /* Same handoff with an explicit engine: TK_SEND_AUTO (= tk_kv_send: the SM
- * page-copy kernel when src can address dst's pool, else the copy engine),
+ * page-copy kernel when src and dst share a device, the copy engines across
+ * devices -- the NVLink transfer then leaves the SMs to the next chunk),
  * TK_SEND_SM (kernel on src's SMs: peer stores over NVLink / device copy),
  * TK_SEND_CE (copy engines: one async copy per run of consecutive pages;
  * leaves the SMs to the next chunk).  Replaces the same stand-in,

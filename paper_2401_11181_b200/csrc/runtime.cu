@@ -1129,7 +1129,12 @@ int tk_kv_send_ex(tk_instance* src, const int32_t* src_pages, tk_instance* dst,
   if (!peer) TK_CUDA(cudaDeviceCanAccessPeer(&peer, src->device, dst->device));
   TK_CHECK(peer || engine != TK_SEND_SM, TK_EINVAL,
            "tk_kv_send: TK_SEND_SM needs peer access from src to dst");
-  if (peer && engine != TK_SEND_CE) {
+  // AUTO: the page-copy kernel for a device-local handoff (co-located P and D: 2.2 vs
+  // 4.2 ms for 8k tokens, the copy engines starve beside the chunk's GEMMs), the copy
+  // engines across devices: the NVLink transfer then takes no SMs from the next chunk
+  // (bench kv_handoff_nvlink / overlap_nvlink measure both engines).
+  const bool use_sm = engine == TK_SEND_SM || (engine == TK_SEND_AUTO && src->device == dst->device);
+  if (peer && use_sm) {
     // one copy kernel on the source GPU; a peer destination is written over NVLink
     int sms = 0;
     TK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, src->device));

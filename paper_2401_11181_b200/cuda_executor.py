@@ -124,7 +124,8 @@ class CudaExecutor:
         self.staging_pages = int(mcfg.get("staging_pages", 512))
         self.max_batch = int(mcfg.get("max_decode_batch", 256))
         self.device_predictor = bool(mcfg.get("device_predictor", True))
-        # handoff engine: "auto" (SM page-copy kernel, peer stores over NVLink),
+        # handoff engine: "auto" (SM page-copy kernel on one device, copy engines
+        # over NVLink across devices),
         # "sm", or "ce" (copy engines, leaves the SMs to the next chunk)
         self.send_engine = str(mcfg.get("kv_send_engine", "auto"))
         if self.send_engine not in native.SEND_ENGINES:
