@@ -145,9 +145,9 @@ def measured_peaks() -> dict:
 
 def gemm_traffic(prof: dict):
     """DRAM bytes per GEMM launch (dram__bytes_read.sum + dram__bytes_write.sum from the
-    committed ncu --set full captures, profiles/r01_gemm_traffic.json), weighted by this
-    run's launches of each shape, next to the algorithmic bytes of the same launches."""
-    p = ROOT / "profiles" / "r01_gemm_traffic.json"
+    committed ncu --set full capture of an in-situ layer, profiles/r02_gemm_traffic.json),
+    weighted by this run's launches of each shape, next to the algorithmic bytes."""
+    p = ROOT / "profiles" / "r02_gemm_traffic.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text())
@@ -158,7 +158,7 @@ def gemm_traffic(prof: dict):
     dram = sum(prof[k]["launches"] * d["dram_bytes_per_launch"][v] for k, v in kinds.items()) / n
     alg = sum(prof[k]["launches"] * d["algorithmic_bytes_per_launch"][v] for k, v in kinds.items()) / n
     return {"dram_bytes_per_launch": int(dram), "algorithmic_bytes_per_launch": int(alg),
-            "ratio": round(dram / alg, 3), "source": "profiles/r01_gemm_traffic.json (M=512 shapes)"}
+            "ratio": round(dram / alg, 3), "source": "profiles/r02_gemm_traffic.json (M=512 shapes, in situ)"}
 
 
 # ---------------------------------------------------------------- CPU port (oracle)
