@@ -138,8 +138,14 @@ def check(rc: int, what: str = "") -> int:
 
 
 def i32(values) -> C.Array:
-    vals = list(values)
-    return (C.c_int32 * max(1, len(vals)))(*vals)
+    """int32 C array from a sequence (array.array fills it in C: a decode step's
+    block table of ~20k entries converts in ~0.4 ms instead of ~3 ms through
+    ctypes argument unpacking)."""
+    import array
+    buf = array.array("i", values)
+    if not buf:
+        return (C.c_int32 * 1)()
+    return (C.c_int32 * len(buf)).from_buffer(buf)  # keeps `buf` alive
 
 
 # ---------------------------------------------------------------- model shapes
