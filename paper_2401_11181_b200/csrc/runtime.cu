@@ -600,8 +600,32 @@ int tk_instance_create(int32_t device, const tk_model_desc* model, uint64_t seed
   TK_CUDA(cudaStreamCreateWithFlags(&inst->s_pred, cudaStreamNonBlocking));
   const int64_t rows = max_chunk;
   const int ffn_cols = m.arch == TK_ARCH_OPT ? m.ffn : 3 * m.ffn;
-  TK_CUDA(cudaMalloc(&inst->resid, rows * m.hidden * 4));
-  TK_CUDA(cudaMalloc(&inst->delta, rows * m.hidden * 2));
+  // The fp32 residual stream and the pending bf16 update are one allocation;
+  // TK_L2_PERSIST=1 keeps it in a persisting L2 window on the compute stream (the
+  // add+norm re-reads both after the weight stream and the KV pages went through
+  // L2).  Off by default: in situ the norms gain <1% (they are bound by their
+  // launch ramp and tail, not by DRAM; profiles/r02_experiments.md).
+  TK_CUDA(cudaMalloc(&inst->resid, rows * m.hidden * 6));
+  inst->delta = reinterpret_cast<__nv_bfloat16*>(inst->resid + rows * m.hidden);
+  {
+    static const bool persist = getenv("TK_L2_PERSIST") && atoi(getenv("TK_L2_PERSIST")) != 0;
+    cudaDeviceProp prop{};
+    TK_CUDA(cudaGetDeviceProperties(&prop, device));
+    const size_t want = static_cast<size_t>(rows) * m.hidden * 6;
+    if (persist && prop.persistingL2CacheMaxSize > 0 && prop.accessPolicyMaxWindowSize > 0) {
+      size_t cur = 0;
+      TK_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+      const size_t lim = std::min<size_t>(prop.persistingL2CacheMaxSize, cur + want);
+      TK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+      cudaStreamAttrValue attr{};
+      attr.accessPolicyWindow.base_ptr = inst->resid;
+      attr.accessPolicyWindow.num_bytes = std::min<size_t>(want, prop.accessPolicyMaxWindowSize);
+      attr.accessPolicyWindow.hitRatio = 1.0f;
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      TK_CUDA(cudaStreamSetAttribute(inst->s_compute, cudaStreamAttributeAccessPolicyWindow, &attr));
+    }
+  }
   TK_CUDA(cudaMalloc(&inst->xn, rows * m.hidden * 2));
   // qkv scratch doubles as the fp32 gather buffer of the head
   TK_CUDA(cudaMalloc(&inst->qkv, rows * std::max<int64_t>(3 * m.hidden * 2, m.hidden * 4)));
@@ -662,8 +686,7 @@ int tk_instance_destroy(tk_instance* inst) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   cudaFree(inst->dec_fixed);
   cudaFree(inst->pool);
-  cudaFree(inst->resid);
-  cudaFree(inst->delta);
+  cudaFree(inst->resid);  // (delta lives in the same allocation)
   cudaFree(inst->xn);
   cudaFree(inst->qkv);
   cudaFree(inst->attn);
@@ -801,8 +824,10 @@ static int prefill_impl(tk_instance* inst, cudaStream_t s, int32_t n_tokens,
     // attention CTAs (TK_FA_CTAS caps them, experiments)
     static const int fa_ctas = getenv("TK_FA_CTAS") ? std::max(1, std::min(kNumSMs, atoi(getenv("TK_FA_CTAS"))))
                                                     : kNumSMs;
-    TK_CHECK(build_fa_plan(slices, n_slices, m.n_heads, fa_ctas, &fa, pairs, pcap, units, ucap,
-                           groups, pcap * m.n_heads, off, kNumSMs + 1) == 0,
+    const int span = fa_span(m.head_dim);
+    TK_CHECK(build_fa_plan(slices, n_slices, m.n_heads, span > 256 ? fa_ctas / 2 : fa_ctas, &fa,
+                           pairs, pcap, units, ucap, groups, pcap * m.n_heads, off, kNumSMs + 1,
+                           span) == 0,
              TK_EINVAL, "prefill: attention plan overflow");
   } else {
     const int qcap = n_slices + n_tokens / 128 + 1;
@@ -1398,9 +1423,10 @@ static int chunk_attention_impl(const void* q, int32_t q_stride, void* o, const 
     std::vector<FaUnit> units(ucap);
     std::vector<FaGroup> groups(pcap * n_heads);
     std::vector<int32_t> off(kNumSMs + 1);
-    TK_CHECK(build_fa_plan(slices, n_slices, n_heads, kNumSMs, &fa, pairs.data(), pcap,
-                           units.data(), ucap, groups.data(), pcap * n_heads, off.data(),
-                           kNumSMs + 1) == 0,
+    const int span = fa_span(head_dim);
+    TK_CHECK(build_fa_plan(slices, n_slices, n_heads, span > 256 ? kNumSMs / 2 : kNumSMs, &fa,
+                           pairs.data(), pcap, units.data(), ucap, groups.data(), pcap * n_heads,
+                           off.data(), kNumSMs + 1, span) == 0,
              TK_EINVAL, "tk_chunk_attention: attention plan overflow");
     d_pairs = upload(pairs.data(), pairs.size() * sizeof(FaPair));
     d_units = upload(units.data(), units.size() * sizeof(FaUnit));

@@ -489,6 +489,52 @@ __device__ __forceinline__ void umma_bf16_ts_k64(uint32_t d_tmem, uint32_t a_tme
       : "memory");
 }
 
+// cta_group::2 forms of the two panels above, issued by the even CTA of a pair:
+// A (each CTA's 128 rows) and D (each CTA's TMEM) at the same offsets in both
+// CTAs, B split along N (each CTA holds N/2 at the same offset).
+template <uint32_t kHalfUnitsA, uint32_t kHalfUnitsB>
+__device__ __forceinline__ void umma_bf16_pair_k128(uint32_t d_tmem, uint64_t a_desc,
+                                                    uint64_t b_desc, uint32_t idesc,
+                                                    uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 a, b;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.s64 a, %1, 2;\n\tadd.s64 b, %2, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 4;\n\tadd.s64 b, %2, 4;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 6;\n\tadd.s64 b, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, %5;\n\tadd.s64 b, %2, %6;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "n"(kHalfUnitsA), "n"(kHalfUnitsB)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16_pair_ts_k64(uint32_t d_tmem, uint32_t a_tmem,
+                                                      uint64_t b_desc, uint32_t idesc,
+                                                      uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "add.u32 a, %1, 8;\n\tadd.s64 b, %2, 128;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t"
+      "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t"
+      "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }

@@ -121,11 +121,14 @@ struct FaGroup {                       // a (pair, head) computed as several pie
 };
 struct FaPlan {
   int n_pairs, n_units, n_ctas, n_pieces, n_groups;
+  int span;  // query rows per record: 256 (pairs, one CTA per unit) / 512 (quads, CTA pairs)
 };
 // Host-side plan; arrays are caller-provided with capacities.  0 / -1 (overflow).
 int build_fa_plan(const tk_slice* slices, int n_slices, int n_heads, int max_ctas, FaPlan* plan,
                   FaPair* pairs, int pcap, FaUnit* units, int ucap, FaGroup* groups, int gcap,
-                  int32_t* cta_off, int ocap);
+                  int32_t* cta_off, int ocap, int span = 256);
+// Record span the attention launch for this head_dim uses (512: CTA-pair kernel).
+int fa_span(int head_dim);
 int64_t fa_partial_bytes();
 int gemm_debug_trace(unsigned long long* host, int n);
 int gemm_debug_cta_trace(unsigned long long* host, int n);

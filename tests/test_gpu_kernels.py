@@ -291,6 +291,31 @@ def test_chunk_attention_long_prefix_pieces(prefix, n, H, D):
           f"min cos {worst[1]:.6f}")
 
 
+@pytest.mark.parametrize("reqs,H", [([(394, 118), (0, 18), (0, 100), (0, 276)], 4),
+                                     ([(0, 512)], 40), ([(2048, 512)], 40), ([(7680, 512)], 8),
+                                     ([(130, 77)], 40), ([(256, 300)], 3), ([(3000, 700)], 5)])
+def test_chunk_attention_cta_pair_kernel(monkeypatch, reqs, H):
+    """The cta_group::2 form of the chunk attention (TK_FA_PAIR=1: 512-row quads,
+    M=256 pair MMAs, each CTA holding half of every K/V block): mixed slices,
+    short and long prefixes (stream-K pieces over four sub-tiles), ragged quads,
+    with the same negative controls as the single-CTA kernel."""
+    monkeypatch.setenv("TK_FA_PAIR", "1")
+    L, D, pt, layer = 2, 128, 16, 1
+    pool, bt, slices, qkv, spare = _chunk_case(reqs, H, 7, L, D, pt)
+    o = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bt, pt)
+    torch.cuda.synchronize()
+    worst = _check_chunk(o, qkv, pool, bt, slices, layer, H, D, pt)
+    prefix = reqs[0][0]
+    if prefix >= 256:
+        bad_bt = list(bt)
+        for i in range(8):
+            bad_bt[(prefix // 2) // pt + i] = spare[i % len(spare)] if spare else bt[0]
+        o_bad = native.chunk_attention(qkv, 3 * H * D, pool, layer, L, H, D, slices, bad_bt, pt)
+        with pytest.raises(AssertionError):
+            _check_chunk(o_bad, qkv, pool, bt, slices[:1], layer, H, D, pt, negative=False)
+    print(f"cta-pair chunk attention {reqs} H {H}: max rel {worst[0]:.2e}, min cos {worst[1]:.6f}")
+
+
 def test_gemm_shared_workspace_across_shapes():
     """One workspace serves every GEMM shape of a layer (as in the runtime)."""
     import ctypes
