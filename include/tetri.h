@@ -239,10 +239,13 @@ int tk_chunk_attention_timed(const void* q, int32_t q_stride, void* o, const voi
 /* The chunk-attention work plan for a chunk's slices (host only, no device):
  * counts = {pairs, units, ctas, pieces, split groups}; pairs[i*6..] = (slice,
  * row0, pos0, nrows0, nrows1, key blocks); units[i*5..] = (pair, head, kb0,
- * kb1, piece); cta_off[c] = first unit of CTA c (n_ctas + 1 entries).       */
+ * kb1, piece); cta_off[c] = first unit of CTA c (n_ctas + 1 entries).
+ * span 256: records are pairs of 128-row tiles, one CTA per unit; span 512:
+ * quads of the CTA-pair kernel (nrows0 = the quad's rows, nrows1 = 0), one
+ * 2-CTA cluster per unit -- max_ctas / ctas then count clusters.            */
 int tk_fa_plan(const tk_slice* slices, int32_t n_slices, int32_t n_heads, int32_t max_ctas,
                int32_t* counts, int32_t* pairs, int32_t pair_cap, int32_t* units,
-               int32_t unit_cap, int32_t* cta_off, int32_t cta_cap);
+               int32_t unit_cap, int32_t* cta_off, int32_t cta_cap, int32_t span);
 /* Debug: clock64 stamps of the chunk-attention pipeline of CTA 0, recorded
  * only when TK_FA_VARIANT=7 (scripts/attn_trace.py).                       */
 int tk_debug_fa_trace(uint64_t* host, int32_t n);

@@ -1509,15 +1509,16 @@ int tk_chunk_attention_timed(const void* q, int32_t q_stride, void* o, const voi
 
 int tk_fa_plan(const tk_slice* slices, int32_t n_slices, int32_t n_heads, int32_t max_ctas,
                int32_t* counts, int32_t* pairs, int32_t pcap, int32_t* units, int32_t ucap,
-               int32_t* cta_off, int32_t ocap) {
+               int32_t* cta_off, int32_t ocap, int32_t span) {
   TK_CHECK(slices && counts && pairs && units && cta_off && n_slices > 0, TK_EINVAL,
            "tk_fa_plan: arguments");
   FaPlan plan{};
   std::vector<FaPair> pr(pcap);
   std::vector<FaUnit> un(ucap);
   std::vector<FaGroup> gr(std::max(1, ucap));
+  TK_CHECK(span == 256 || span == 512, TK_EINVAL, "tk_fa_plan: span 256 or 512");
   TK_CHECK(build_fa_plan(slices, n_slices, n_heads, max_ctas, &plan, pr.data(), pcap, un.data(),
-                         ucap, gr.data(), ucap, cta_off, ocap) == 0,
+                         ucap, gr.data(), ucap, cta_off, ocap, span) == 0,
            TK_EINVAL, "tk_fa_plan: capacity");
   counts[0] = plan.n_pairs;
   counts[1] = plan.n_units;

@@ -96,7 +96,7 @@ _SIGNATURES = {
     "tk_debug_gemm_trace": ([C.POINTER(C.c_uint64), C.c_int32], C.c_int),
     "tk_debug_gemm_cta_trace": ([C.POINTER(C.c_uint64), C.c_int32], C.c_int),
     "tk_fa_plan": ([C.POINTER(tk_slice), C.c_int32, C.c_int32, C.c_int32, _I32P, _I32P, C.c_int32,
-                    _I32P, C.c_int32, _I32P, C.c_int32], C.c_int),
+                    _I32P, C.c_int32, _I32P, C.c_int32, C.c_int32], C.c_int),
     "tk_chunk_attention_timed": ([_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int32, C.POINTER(tk_slice), C.c_int32, _I32P,
                                   C.c_int32, C.c_float, _P, C.c_int32, C.POINTER(C.c_float)],
@@ -581,8 +581,9 @@ def chunk_attention_timed(q, q_stride, pool, layer, n_layers, n_heads, head_dim,
     return o, us.value
 
 
-def fa_plan(slices, n_heads, max_ctas=148):
-    """Chunk-attention work plan (host only): (pairs, units, cta_off, n_pieces)."""
+def fa_plan(slices, n_heads, max_ctas=148, span=256):
+    """Chunk-attention work plan (host only): (pairs, units, cta_off, n_pieces).
+    span 512: the CTA-pair kernel's quads, max_ctas counting 2-CTA clusters."""
     n = len(slices)
     n_tok = sum(sl[1] for sl in slices)
     pcap = n + n_tok // 256 + 1
@@ -593,7 +594,7 @@ def fa_plan(slices, n_heads, max_ctas=148):
     off = (C.c_int32 * (max_ctas + 1))()
     sl = (tk_slice * n)(*[tk_slice(*x) for x in slices])
     check(load().tk_fa_plan(sl, n, n_heads, max_ctas, counts, pairs, pcap, units, ucap, off,
-                            max_ctas + 1), "tk_fa_plan")
+                            max_ctas + 1, span), "tk_fa_plan")
     n_pairs, n_units, n_ctas, n_pieces = counts[0], counts[1], counts[2], counts[3]
     return ([tuple(pairs[i * 6:(i + 1) * 6]) for i in range(n_pairs)],
             [tuple(units[i * 5:(i + 1) * 5]) for i in range(n_units)],
