@@ -153,10 +153,14 @@ def test_opt13b_width_reference_prompts():
     inst.close()
 
 
-def test_opt13b_width_c2_round():
+@pytest.mark.parametrize("pair_attention", [False, True], ids=["attn1cta", "attn2cta"])
+def test_opt13b_width_c2_round(monkeypatch, pair_attention):
     """One full C2 scheduling round at OPT-13B width (144 chunks of 512, prefixes
     to 7680): the benchmark's own chunk layout, first-token logits of all 16
-    prompts, KV pages deep in the 8192-token prompt, then decode at ctx <= 8193."""
+    prompts, KV pages deep in the 8192-token prompt, then decode at ctx <= 8193.
+    attn2cta: the same round through the CTA-pair chunk attention (TK_FA_PAIR=1)."""
+    if pair_attention:
+        monkeypatch.setenv("TK_FA_PAIR", "1")
     m = OPT13B_2L
     _, rounds = bench.build_workload(0)
     batch, chunks = rounds[0]
@@ -179,7 +183,7 @@ def test_opt13b_width_c2_round():
     assert page_err < 2e-2, page_err
     d_err, d_dec, d_rows = _decode_both(inst, ora, cache, rids, [int(v) for v in ref.argmax(-1)],
                                         [lens[r] for r in rids], tables, 2)
-    record("opt13b_width_c2_round", chunks=len(chunks), prefill_max_err=err, prefill_min_cos=cos,
+    record("opt13b_width_c2_round" + ("_cta_pair" if pair_attention else ""), chunks=len(chunks), prefill_max_err=err, prefill_min_cos=cos,
            prefill_decided=decided, kv_page_rel_err=page_err, decode_max_err=d_err,
            decode_decided=d_dec, decode_rows=d_rows)
     assert decided >= 8 and d_dec >= d_rows // 2, (decided, d_dec, d_rows)
